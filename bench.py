@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark: NFFT trafo+adjoint nodes/sec on B200 (BASELINE.json metric).
+
+One step = one forward transform (D -> F -> B) plus one adjoint
+(B^H -> F^H -> D^H) over the configuration's M nodes on every rank.
+
+* ``value``  : whole-job nodes/s with inputs resident in HBM, device-timed
+               (CUDA events on the launching stream, max over ranks), L2 flushed
+               (256 MiB write) before every timed step.
+* ``e2e``    : same metric through the reference-facing C-ABI with HOST
+               buffers (nfftk_set_fhat / nfftk_trafo / nfftk_set_f /
+               nfftk_adjoint: H2D + compute + D2H inside the timed region).
+* ``roofline``: dominant gridding kernel (interp / spread) against measured HBM.
+* ``cpu_baseline``: the CPU oracle port of the reference (oracle/), all host
+               threads, bounded sample, rank 0 at N=1.
+
+``--impl reference`` times only that CPU port (rank 0; other ranks exit 0).
+Multi-GPU (torchrun): weak scaling, each rank owns M nodes of one plan; the
+adjoint all-reduces the spread grid with NCCL (paper_1810_09891_b200.distributed).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1810_09891_b200 import workloads as wl  # noqa: E402
+
+DEFAULT_CONFIG = "C3"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(wl.CONFIGS))
+    ap.add_argument("--precision", default="double", choices=["double", "single"])
+    ap.add_argument("--psi", default="flags", choices=["flags", "direct", "tensor"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def config_json(w, args, world):
+    return {
+        "workload": f"{w.name}: d={w.d} N={'x'.join(map(str, w.N))} n={'x'.join(map(str, w.n))} "
+                    f"M={w.M} per rank m={w.m} {w.dist} nodes, Kaiser-Bessel",
+        "d": w.d, "N": list(w.N), "n": list(w.n), "M_per_rank": w.M, "m": w.m,
+        "nodes": w.dist, "window": "kaiserbessel", "flags": "default f1 (PRE_PHI_HUT|PRE_PSI|sort)"
+        if args.psi == "flags" else f"psi={args.psi}",
+        "step": "trafo + adjoint", "parallelism": f"node-sharded x{world}",
+        "l2": "flushed (256 MiB write) before every timed step",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_oracle_rate(w, seconds, seed_offset=0):
+    """Time the CPU oracle port (trafo + adjoint) on a bounded node sample.
+
+    The sample keeps the grid, cutoff and node distribution and scales M down
+    until one trafo+adjoint takes a bounded time; the rate is nodes/s of the
+    full step (deconvolution + FFT + gridding) at that M.
+    """
+    from oracle import oracle as O
+
+    threads = O.max_threads()
+    M = w.M
+    base = wl.scaled(w, M)
+    # probe with a small sample, then size the measured sample
+    probe = wl.scaled(w, min(M, 16384))
+    x = wl.nodes(probe, seed=wl.NODE_SEED + seed_offset)
+    fh = wl.fhat(probe)
+    fs = wl.samples(probe)
+    t0 = time.perf_counter()
+    O.trafo(w.N, w.n, w.m, x, fh)
+    O.adjoint(w.N, w.n, w.m, x, fs)
+    t_probe = time.perf_counter() - t0
+    target = max(1.0, seconds / 3.0)
+    Ms = M if t_probe * M / probe.M < target else max(probe.M, int(probe.M * target / max(t_probe, 1e-3)))
+    Ms = min(M, Ms)
+    samp = wl.scaled(base, Ms)
+    x = wl.nodes(samp, seed=wl.NODE_SEED + seed_offset)
+    fh = wl.fhat(samp)
+    fs = wl.samples(samp)
+    reps, elapsed = 0, 0.0
+    while reps < 3 and elapsed < seconds:
+        t0 = time.perf_counter()
+        O.trafo(w.N, w.n, w.m, x, fh)
+        O.adjoint(w.N, w.n, w.m, x, fs)
+        elapsed += time.perf_counter() - t0
+        reps += 1
+    rate = Ms * reps / elapsed
+    sample = (f"oracle/ C port (OpenMP) of reference trafo+adjoint, {reps} step(s) at M={Ms}"
+              f" of {M} (same grid/cutoff/distribution), {threads} threads")
+    return rate, threads, sample
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    w = wl.CONFIGS[args.config]
+    from oracle import oracle as O
+
+    threads = O.max_threads()
+    x = wl.nodes(w)
+    fh = wl.fhat(w)
+    fs = wl.samples(w)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.trafo(w.N, w.n, w.m, x, fh)
+        O.adjoint(w.N, w.n, w.m, x, fs)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = w.M / (ms / 1000.0)
+    line = {
+        "metric": "NFFT trafo+adjoint nodes/sec", "value": value, "unit": "nodes/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded, SURVEY 8(d) generators)", "impl": "reference",
+        "config": config_json(w, args, 1),
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "port",
+                         "sample": f"full {w.name} workload (M={w.M}) per step, oracle/ C port "
+                                   f"of the reference path, {threads} OpenMP threads"},
+        "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU legs
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_09891_b200 as nf
+    from paper_1810_09891_b200 import _lib
+    from paper_1810_09891_b200.distributed import DistributedPlan
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = wl.CONFIGS[args.config]
+    cdt = torch.complex64 if args.precision == "single" else torch.complex128
+    s_elem = 8 if args.precision == "single" else 16
+
+    # ---- plan over this rank's shard (weak scaling: M nodes per rank)
+    dp = DistributedPlan(w.N, w.M, n=w.n, m=w.m, precision=args.precision, device=dev)
+    plan = dp.plan
+    if args.psi != "flags":
+        plan.set_psi_policy(nf.MODE_DIRECT if args.psi == "direct" else nf.MODE_TENSOR)
+    x = torch.from_numpy(wl.nodes(w, seed=wl.NODE_SEED + rank)).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dp.set_nodes(x)
+    dp.precompute()
+    torch.cuda.synchronize()
+    precompute_ms = 1000 * (time.perf_counter() - t0)
+    fhat = torch.from_numpy(wl.fhat(w)).to(dev, cdt)
+    fsamp = torch.from_numpy(wl.samples(w, seed=wl.F_SEED + rank)).to(dev, cdt)
+    f_out = torch.empty(w.M, dtype=cdt, device=dev)
+    fhat_out = torch.empty(w.num_freqs, dtype=cdt, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        plan.trafo(fhat, out=f_out)
+        dp.adjoint(fsamp, out=fhat_out)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region
+    plan.phase_times(reset=True)
+    plan.set_timing(True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = nf.launch_count()
+    stream = torch.cuda.current_stream()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        b.synchronize()
+        total_ms += a.elapsed_time(b)
+    torch.cuda.synchronize()
+    launches = nf.launch_count() - launches0
+    clk = clocks.stop()
+    plan.set_timing(False)
+    phases = plan.phase_times(reset=True)
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    value = world * w.M / (ms_per_step / 1000.0)
+
+    # ---- e2e through the reference-facing C-ABI with host buffers
+    e2e = e2e_abi(w, args, rank, world, dp, dev, cdt)
+
+    # ---- roofline of the dominant gridding kernel
+    peaks = measured_peaks()
+    fp64, fp32 = ctypes_fma_peaks(_lib)
+    roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": "NFFT trafo+adjoint nodes/sec", "value": value, "unit": "nodes/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64" if args.precision == "single" else "c128",
+        "data": "synthetic (seeded, SURVEY 8(d) generators)",
+        "config": config_json(w, args, world),
+        "e2e": e2e,
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
+        "precompute_ms": precompute_ms,
+        "fma_peaks_tflops": {"fp64": fp64, "fp32": fp32},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample = cpu_oracle_rate(w, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "nodes/s", "cores": cores, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_abi(w, args, rank, world, dp, dev, cdt):
+    """Host-buffer end-to-end rate.  N=1: the reference C-ABI (set_fhat/trafo,
+    set_f/adjoint) whose buffers are library-owned pinned memory.  N>1: the
+    distributed API with pinned host tensors copied in and out every step."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_09891_b200 import _lib
+
+    fh = np.ascontiguousarray(wl.fhat(w)).view(np.float64)
+    fs = np.ascontiguousarray(wl.samples(w, seed=wl.F_SEED + rank)).view(np.float64)
+    h2d = 16 * (w.num_freqs + w.M) if args.precision == "double" else 8 * (w.num_freqs + w.M)
+    d2h = h2d
+    steps = max(3, min(args.steps, 10))
+    if world == 1 and args.precision == "double":
+        lib = _lib.load()
+        N = _lib.i32_array(w.N)
+        n = _lib.i32_array(w.n)
+        flags = 0x1fd1 if w.d > 1 else 0xfd1
+        h = lib.nfftk_create_advanced(N, w.d, w.M, n, w.m, flags, 0x41)
+        assert h > 0, h
+        x = np.ascontiguousarray(wl.nodes(w))
+        assert lib.nfftk_set_x(h, x.ctypes.data, x.size) == 0, lib.nfftk_last_error_message(h)
+
+        def one():
+            rc = lib.nfftk_set_fhat(h, fh.ctypes.data, fh.size) or lib.nfftk_trafo(h)
+            rc = rc or lib.nfftk_set_f(h, fs.ctypes.data, fs.size) or lib.nfftk_adjoint(h)
+            assert rc == 0, lib.nfftk_last_error_message(h)
+            return lib.nfftk_get_f(h), lib.nfftk_get_fhat(h)
+
+        for _ in range(2):
+            one()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        ms = 1000 * (time.perf_counter() - t0) / steps
+        lib.nfftk_destroy(h)
+        path = "C-ABI nfftk_set_fhat+nfftk_trafo+nfftk_set_f+nfftk_adjoint (host buffers)"
+    else:
+        fhh = torch.from_numpy(wl.fhat(w)).to(cdt).pin_memory()
+        fsh = torch.from_numpy(wl.samples(w, seed=wl.F_SEED + rank)).to(cdt).pin_memory()
+        fo = torch.empty(w.M, dtype=cdt).pin_memory()
+        fho = torch.empty(w.num_freqs, dtype=cdt).pin_memory()
+
+        def one():
+            a = fhh.to(dev, non_blocking=True)
+            b = fsh.to(dev, non_blocking=True)
+            fo.copy_(dp.trafo(a), non_blocking=True)
+            fho.copy_(dp.adjoint(b), non_blocking=True)
+            torch.cuda.synchronize()
+
+        for _ in range(2):
+            one()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        ms = 1000 * (time.perf_counter() - t0) / steps
+        path = "Plan/DistributedPlan API with pinned host tensors"
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": world * w.M / (ms / 1000.0), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "path": path, "steps": steps}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "MEASURED_PEAKS.json (measured)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "source": "B200_PROFILING.md fallback"}
+
+
+def ctypes_fma_peaks(_lib):
+    import ctypes
+
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _lib.load().nfftk_measure_fma_peaks(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+def roofline(w, phases, steps, s, peaks, fma_tflops):
+    """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
+    M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
+    (4 w^d M flops with w = 2m)."""
+    ti = phases.get("interp", (0.0, 0))
+    ts = phases.get("spread", (0.0, 0))
+    name, (ms, calls) = ("spread", ts) if ts[0] >= ti[0] else ("interp", ti)
+    if not calls:
+        return None
+    per = ms / calls
+    traffic_alg = w.M * (8 * w.d + s + 4) + s * w.grid_size
+    achieved = traffic_alg / (per * 1e-3) / 1e9
+    flops = 4 * (2 * w.m) ** w.d * w.M
+    tflops = flops / (per * 1e-3) / 1e12
+    return {
+        "kernel": f"k_{name}_tiled", "bound": "hbm", "achieved": achieved,
+        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+        "traffic": None, "algorithmic_bytes_per_launch": traffic_alg,
+        "avg_launch_ms": per, "peak_source": peaks["source"],
+        "fma": {"achieved_tflops": tflops, "peak_tflops": fma_tflops,
+                "frac": tflops / fma_tflops if fma_tflops else None,
+                "flops_per_launch": flops, "peak_source": "k_fma_peak microbenchmark (measured in run)"},
+    }
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,42 @@
+// Host-side launchers for the kernels in kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace nfftk {
+
+struct DeconvGeomH {
+  int d;
+  int N[MAX_D];
+  int n[MAX_D];
+  const double* col[MAX_D];  // device: phi_hat_i(k) * wscale_i for k + N_i/2
+  double grid_size;
+};
+
+unsigned long long launch_count();
+
+void launch_check_range(const double* x, int64_t count, unsigned long long* first_bad,
+                        cudaStream_t s);
+void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int ntiles,
+                  int* perm, double* xs, int* tile_count, int* tile_start, int4** subs,
+                  int* nsubs, cudaStream_t s);
+unsigned long long sum_widths(const double* xs, int64_t M, const Geom& g, cudaStream_t s);
+void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s);
+void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaStream_t s);
+
+void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH& q, cudaStream_t s);
+void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& q, cudaStream_t s);
+void launch_interp(bool single, const void* grid, void* f, const double* xs, const int* perm,
+                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+void launch_spread(bool single, void* grid, const void* f, const double* xs, const int* perm,
+                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+
+double measure_fma_tflops(bool fp64);
+
+size_t interp_smem(const Geom& g, int elem_bytes, int threads);
+size_t spread_smem(const Geom& g, int elem_bytes);
+
+}  // namespace nfftk

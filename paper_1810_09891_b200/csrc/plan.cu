@@ -1,0 +1,588 @@
+// Plan lifecycle and transform orchestration for the B200 NFFT.
+// Parameter validation follows Plan.__init__ (plan.py:138-186) check by check
+// so the ABI reports the same error classes and codes as the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+
+#include "plan.h"
+
+namespace nfftk {
+
+static std::string fmt_tuple(const std::vector<int>& v) {
+  std::ostringstream os;
+  os << "(";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) os << ", ";
+    os << v[i];
+  }
+  if (v.size() == 1) os << ",";
+  os << ")";
+  return os.str();
+}
+
+static std::string fmt_double(double v) {
+  // shortest round-trip representation, like Python's repr(float)
+  char buf[64];
+  for (int prec = 1; prec <= 17; ++prec) {
+    snprintf(buf, sizeof buf, "%.*g", prec, v);
+    if (strtod(buf, nullptr) == v) break;
+  }
+  std::string s(buf);
+  if (s.find_first_of(".eni") == std::string::npos) s += ".0";
+  return s;
+}
+
+static std::string hexs(uint32_t v) {
+  char buf[32];
+  snprintf(buf, sizeof buf, "0x%x", v);
+  return buf;
+}
+
+// ------------------------------------------------------- host window math
+// window.py:38-53
+double host_bessel_i0(double x) {
+  double s = 1.0, t = 1.0, q = 0.25 * x * x;
+  long j = 0;
+  for (;;) {
+    j += 1;
+    t *= q / (double)(j * j);
+    s += t;
+    if (t < 1e-16 * s) return s;
+  }
+}
+
+// window.py:56-72
+double host_window(int code, double t, double n_i, double m, double b_i) {
+  if (code == WINDOW_KB) {
+    double nt = n_i * t;
+    double u = m * m - nt * nt;
+    if (u > 0.0) {
+      double z = std::sqrt(u);
+      return std::sinh(b_i * z) / (M_PI * z);
+    }
+    if (u < 0.0) {
+      double z = std::sqrt(-u);
+      return std::sin(b_i * z) / (M_PI * z);
+    }
+    return b_i / M_PI;
+  }
+  double nt = n_i * t;
+  return std::exp(-nt * nt / b_i) / std::sqrt(M_PI * b_i);
+}
+
+// window.py:142-164 (phi_hat), checked strictly positive
+static double host_phi_hat(const Plan* p, int dim, int k) {
+  int n_i = p->n[dim];
+  double b = p->b[dim];
+  double val;
+  if (p->window == WINDOW_KB) {
+    double c = 2.0 * M_PI * k / n_i;
+    double arg = b * b - c * c;
+    if (arg < 0.0)
+      fail(EK_WINDOW, "kaiserbessel transform vanishes at k=" + std::to_string(k));
+    val = host_bessel_i0(p->m * std::sqrt(arg)) / n_i;
+  } else {
+    double c = M_PI * k / n_i;
+    val = std::exp(-b * c * c) / n_i;
+  }
+  if (!(val > 0.0)) fail(EK_WINDOW, "window transform not positive at k=" + std::to_string(k));
+  return val;
+}
+
+std::vector<double> plan_phi_hut(const Plan* p, int dim) {
+  // phi_hat_table(i, kmax=N_i/2) (window.py:166-171; plan.py:256)
+  std::vector<double> out;
+  int kmax = p->N[dim] / 2;
+  for (int k = -kmax; k <= kmax; ++k) out.push_back(host_phi_hat(p, dim, k));
+  return out;
+}
+
+// ------------------------------------------------------------ lifecycle
+Plan::~Plan() {
+  if (device >= 0) cudaSetDevice(device);
+  if (fft_ready) cufftDestroy(fft);
+  cudaFree(x_dev);
+  cudaFree(xs);
+  cudaFree(perm);
+  cudaFree(tile_count);
+  cudaFree(subs);
+  cudaFree(psi);
+  cudaFree(lut);
+  cudaFree(cols);
+  if (!grid_external) cudaFree(grid);
+  cudaFree(fhat_dev);
+  cudaFree(f_dev);
+  if (fhat_pinned) cudaFreeHost(fhat_host); else free(fhat_host);
+  if (f_pinned) cudaFreeHost(f_host); else free(f_host);
+  for (auto& r : recs) { event_pool.push_back(r.a); event_pool.push_back(r.b); }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// Tile edge per dim: the largest power of two whose (T+2m+1)^d halo fits the
+// shared-memory budget (two CTAs per SM at the default budget).
+static void choose_tiles(Plan* p) {
+  Geom& g = p->geom;
+  size_t budget = (size_t)env_int("NFFTK_HALO_KB", 100) * 1024;
+  int force = env_int("NFFTK_TILE", 0);
+  int start = p->d == 3 ? 16 : (p->d == 2 ? 128 : 4096);
+  int T = start;
+  for (; T > 1; T /= 2) {
+    size_t h = 1;
+    for (int i = 0; i < p->d; ++i) h *= (size_t)(std::min(T, p->n[i]) + 2 * p->m + 1);
+    if (h * p->elem_bytes() <= budget) break;
+  }
+  if (force > 0) T = force;
+  p->ntiles = 1;
+  for (int i = 0; i < p->d; ++i) {
+    g.T[i] = std::min(T, p->n[i]);
+    g.H[i] = g.T[i] + 2 * p->m + 1;
+    g.ntile[i] = (p->n[i] + g.T[i] - 1) / g.T[i];
+    p->ntiles *= g.ntile[i];
+  }
+  p->maxsub = env_int("NFFTK_MAXSUB", 1024);
+}
+
+static void fill_geom(Plan* p) {
+  Geom& g = p->geom;
+  memset(&g, 0, sizeof g);
+  g.d = p->d;
+  g.m = p->m;
+  g.md = (double)p->m;
+  g.code = p->window;
+  g.M = p->M;
+  for (int i = 0; i < p->d && i < MAX_D; ++i) {
+    g.n[i] = p->n[i];
+    g.nd[i] = (double)p->n[i];
+    g.b[i] = p->b[i];
+    g.wscale[i] = p->wscale[i];
+  }
+  if (p->d <= MAX_D) choose_tiles(p);
+}
+
+Plan* plan_create(const std::vector<int>& N_in, int64_t M, const int* n_opt, const int* m_opt,
+                  const uint32_t* f1_opt, const uint32_t* f2_opt, int window, bool single) {
+  // validate_bandlimit (indexing.py:18-29)
+  if (N_in.empty()) fail(EK_BANDLIMIT, "bandlimit vector is empty");
+  for (int v : N_in)
+    if (v < 2 || v % 2 != 0)
+      fail(EK_BANDLIMIT, "bandlimit entries must be even and >= 2, got " + std::to_string(v));
+  if (M < 1) fail(EK_NFFT, "node count must be >= 1, got " + std::to_string(M));
+  if (window != WINDOW_KB && window != WINDOW_GAUSS)
+    fail(EK_NFFT, "unknown window; use 'kaiserbessel' or 'gaussian'");
+  if (M > 0x7fffffffLL) fail(EK_NFFT, "node count must fit in int32");
+  Plan* p = new Plan();
+  p->N = N_in;
+  p->d = (int)N_in.size();
+  p->M = M;
+  p->window = window;
+  p->single = single;
+  try {
+    // plan.py:144-167
+    if (!n_opt) {
+      for (int v : N_in) {
+        int b = 0;
+        while ((1 << b) < v) ++b;   // (v-1).bit_length()
+        p->n.push_back(1 << (b + 1));
+      }
+      if (!m_opt)
+        for (int& v : p->n)
+          while (v < 2 * DEFAULT_CUTOFF + 2) v *= 2;
+    } else {
+      p->n.assign(n_opt, n_opt + p->d);
+      for (int i = 0; i < p->d; ++i) {
+        if (p->n[i] % 2 != 0)
+          fail(EK_OVERSAMPLING, "FFT lengths must be even, got " + std::to_string(p->n[i]));
+        if (p->n[i] <= p->N[i])
+          fail(EK_OVERSAMPLING, "need n_i > N_i, got n=" + fmt_tuple(p->n) + " for N=" + fmt_tuple(p->N));
+      }
+    }
+    int nmin = *std::min_element(p->n.begin(), p->n.end());
+    // plan.py:168-176
+    p->m = !m_opt ? std::min(DEFAULT_CUTOFF, (nmin - 1) / 2) : *m_opt;
+    if (p->m < 1) fail(EK_CUTOFF, "cutoff must be >= 1, got " + std::to_string(p->m));
+    if (2 * p->m + 1 > nmin)
+      fail(EK_CUTOFF, "cutoff " + std::to_string(p->m) + " needs 2m+1 <= min(n) = " + std::to_string(nmin));
+    if (p->m > 16) fail(EK_CUTOFF, "cutoff " + std::to_string(p->m) + " above the supported maximum 16");
+    // plan.py:95-106, :177-178
+    if (f1_opt) {
+      uint32_t f1 = *f1_opt;
+      uint32_t unknown = f1 & ~KNOWN_F1;
+      if (unknown) fail(EK_FLAG, "unknown f1 bits: " + hexs(unknown));
+      if (f1 & UNSUPPORTED_F1)
+        fail(EK_UNSUPPORTED_FLAG, "fast Gaussian gridding flags (FG_PSI, PRE_FG_PSI) are not provided");
+      p->f1 = f1;
+    } else {
+      p->f1 = PRE_PHI_HUT | PRE_PSI | NFFT_SORT_NODES | NOOP_F1 |
+              (p->d > 1 ? NFFT_OMP_BLOCKWISE_ADJOINT : 0);
+    }
+    p->f2 = f2_opt ? *f2_opt : DEFAULT_F2;
+    // WindowModel.make (window.py:91-112)
+    for (int i = 0; i < p->d; ++i) {
+      double s = (double)p->n[i] / (double)p->N[i];
+      if (s <= 1.0) fail(EK_NFFT, "oversampling factor must exceed 1");
+      if ((double)p->m / p->n[i] >= 0.5) fail(EK_NFFT, "window support m/n must be below 1/2");
+      p->sigma.push_back(s);
+      p->b.push_back(window == WINDOW_KB ? M_PI * (2.0 - 1.0 / s)
+                                         : 2.0 * s * p->m / ((2.0 * s - 1.0) * M_PI));
+      // complex64 keeps window products in range by normalising by phi(0)
+      p->wscale.push_back(single ? 1.0 / host_window(window, 0.0, p->n[i], p->m, p->b[i]) : 1.0);
+    }
+    p->num_freqs = 1;
+    p->grid_size = 1;
+    for (int i = 0; i < p->d; ++i) {
+      p->num_freqs *= p->N[i];
+      p->grid_size *= p->n[i];
+    }
+    if (p->d <= MAX_D && p->grid_size > (int64_t)0xffffffffLL)
+      fail(EK_NFFT, "oversampled grid larger than 2^32 cells is not supported");
+    if (cudaGetDevice(&p->device) != cudaSuccess) { p->device = 0; cudaGetLastError(); }
+    fill_geom(p);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+static void ensure_stream(Plan* p) {
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  if (!p->own_stream) NFFTK_CUDA(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+}
+
+// ---------------------------------------------------------- phase events
+struct PhaseScope {
+  Plan* p;
+  int ph;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  static cudaEvent_t take(Plan* p) {
+    cudaEvent_t e;
+    if (!p->event_pool.empty()) {
+      e = p->event_pool.back();
+      p->event_pool.pop_back();
+    } else {
+      NFFTK_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  }
+  PhaseScope(Plan* p_, int ph_, cudaStream_t s_) : p(p_), ph(ph_), s(s_) {
+    if (!p->timing) return;
+    a = take(p);
+    b = take(p);
+    cudaEventRecord(a, s);
+  }
+  ~PhaseScope() {
+    if (!p->timing) return;
+    cudaEventRecord(b, s);
+    p->recs.push_back({ph, a, b});
+  }
+};
+
+void plan_phase_times(Plan* p, double* ms, int64_t* calls, int nmax, int reset) {
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  for (auto& r : p->recs) {
+    NFFTK_CUDA(cudaEventSynchronize(r.b));
+    float t = 0;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    p->phase_ms[r.phase] += t;
+    p->phase_calls[r.phase] += 1;
+    p->event_pool.push_back(r.a);
+    p->event_pool.push_back(r.b);
+  }
+  p->recs.clear();
+  for (int i = 0; i < nmax && i < PH_COUNT; ++i) {
+    if (ms) ms[i] = p->phase_ms[i];
+    if (calls) calls[i] = p->phase_calls[i];
+  }
+  if (reset)
+    for (int i = 0; i < PH_COUNT; ++i) { p->phase_ms[i] = 0; p->phase_calls[i] = 0; }
+}
+
+// ---------------------------------------------------------------- nodes
+static void check_range_host(const Plan* p, const double* x) {
+  int64_t total = p->M * p->d;
+  for (int64_t q = 0; q < total; ++q) {
+    double v = x[q];
+    if (!(v >= -0.5 && v < 0.5))
+      fail(EK_NODE_RANGE, "node " + std::to_string(q / p->d) + " coordinate " + fmt_double(v) +
+                              " outside [-1/2, 1/2)");
+  }
+}
+
+static void shape_check_x(const Plan* p, int64_t len) {
+  if (len != p->M * p->d)
+    fail(EK_SHAPE, "need " + std::to_string(p->M * p->d) + " coordinates (" + std::to_string(p->M) +
+                       " nodes x " + std::to_string(p->d) + "), got " + std::to_string(len));
+}
+
+// Device part of set_nodes: tile binning + sort + sorted coordinates.
+static void nodes_to_device(Plan* p, cudaStream_t s) {
+  const int64_t M = p->M;
+  if (!p->xs) NFFTK_CUDA(cudaMalloc(&p->xs, sizeof(double) * M * p->d));
+  if (!p->perm) NFFTK_CUDA(cudaMalloc(&p->perm, sizeof(int) * M));
+  if (!p->tile_count) {
+    NFFTK_CUDA(cudaMalloc(&p->tile_count, sizeof(int) * (p->ntiles + 1) * 2));
+    p->tile_start = p->tile_count + p->ntiles + 1;
+  }
+  bin_and_sort(p->x_dev, M, p->geom, p->maxsub, p->ntiles, p->perm, p->xs, p->tile_count,
+               p->tile_start, &p->subs, &p->nsubs, s);
+  p->width_sum = sum_widths(p->xs, M, p->geom, s);
+}
+
+static void invalidate_tables(Plan* p) {
+  p->ready = false;
+  if (p->psi) { cudaFree(p->psi); p->psi = nullptr; }
+}
+
+void plan_set_nodes_host(Plan* p, const double* x, int64_t len) {
+  shape_check_x(p, len);
+  check_range_host(p, x);
+  std::vector<double> copy(x, x + p->M * p->d);
+  if (p->d <= MAX_D) {
+    ensure_stream(p);
+    if (!p->x_dev) NFFTK_CUDA(cudaMalloc(&p->x_dev, sizeof(double) * p->M * p->d));
+    NFFTK_CUDA(cudaMemcpyAsync(p->x_dev, copy.data(), sizeof(double) * p->M * p->d,
+                               cudaMemcpyHostToDevice, p->own_stream));
+    invalidate_tables(p);
+    p->has_nodes = false;
+    nodes_to_device(p, p->own_stream);
+    NFFTK_CUDA(cudaStreamSynchronize(p->own_stream));
+  } else {
+    invalidate_tables(p);
+  }
+  p->x_host.swap(copy);
+  p->has_nodes = true;
+}
+
+void plan_set_nodes_device(Plan* p, const double* x, int64_t len, cudaStream_t s) {
+  shape_check_x(p, len);
+  if (p->d > MAX_D) fail(EK_SHAPE, "fast transforms support d <= 3, got d=" + std::to_string(p->d));
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  unsigned long long* bad = nullptr;
+  unsigned long long first = ~0ULL;
+  NFFTK_CUDA(cudaMallocAsync(&bad, sizeof first, s));
+  NFFTK_CUDA(cudaMemcpyAsync(bad, &first, sizeof first, cudaMemcpyHostToDevice, s));
+  launch_check_range(x, p->M * p->d, bad, s);
+  NFFTK_CUDA(cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, s));
+  NFFTK_CUDA(cudaFreeAsync(bad, s));
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+  if (first != ~0ULL) {
+    double v = 0;
+    NFFTK_CUDA(cudaMemcpy(&v, x + first, sizeof v, cudaMemcpyDeviceToHost));
+    fail(EK_NODE_RANGE, "node " + std::to_string(first / p->d) + " coordinate " + fmt_double(v) +
+                            " outside [-1/2, 1/2)");
+  }
+  if (!p->x_dev) NFFTK_CUDA(cudaMalloc(&p->x_dev, sizeof(double) * p->M * p->d));
+  NFFTK_CUDA(cudaMemcpyAsync(p->x_dev, x, sizeof(double) * p->M * p->d, cudaMemcpyDeviceToDevice, s));
+  invalidate_tables(p);
+  p->has_nodes = false;
+  p->x_host.clear();
+  nodes_to_device(p, s);
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+  p->has_nodes = true;
+}
+
+// ------------------------------------------------------------- precompute
+static void ensure_grid(Plan* p) {
+  if (!p->grid) NFFTK_CUDA(cudaMalloc(&p->grid, p->elem_bytes() * p->grid_size));
+  if (!p->fft_ready) {
+    int nn[MAX_D];
+    for (int i = 0; i < p->d; ++i) nn[i] = p->n[i];
+    cufftResult r = cufftPlanMany(&p->fft, p->d, nn, nullptr, 1, 0, nullptr, 1, 0,
+                                  p->single ? CUFFT_C2C : CUFFT_Z2Z, 1);
+    if (r != CUFFT_SUCCESS) fail(EK_CUDA, "cufftPlanMany failed (" + std::to_string((int)r) + ")");
+    p->fft_ready = true;
+  }
+}
+
+void plan_precompute(Plan* p, cudaStream_t s) {
+  if (!p->has_nodes) fail(EK_STATE, "set nodes before precompute()");
+  if (p->d > MAX_D) {
+    // plan.py:278-279: full tables are limited to d <= 3; others only need host tables
+    if (p->f1 & PRE_FULL_PSI)
+      fail(EK_NFFT, "full window tables support d <= 3, got d=" + std::to_string(p->d));
+    for (int i = 0; i < p->d; ++i) plan_phi_hut(p, i);
+    p->ready = true;
+    return;
+  }
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  // PRE_PHI_HUT: deconvolution columns over k = -N/2 .. N/2-1 (transform.py:44-54);
+  // the device always keeps them (their cost is negligible).
+  std::vector<double> cols;
+  for (int i = 0; i < p->d; ++i) {
+    std::vector<double> t = plan_phi_hut(p, i);
+    for (int k = 0; k < p->N[i]; ++k) cols.push_back(t[k] * p->wscale[i]);
+  }
+  if (!p->cols) NFFTK_CUDA(cudaMalloc(&p->cols, sizeof(double) * cols.size()));
+  NFFTK_CUDA(cudaMemcpyAsync(p->cols, cols.data(), sizeof(double) * cols.size(),
+                             cudaMemcpyHostToDevice, s));
+  p->dq.d = p->d;
+  p->dq.grid_size = (double)p->grid_size;
+  size_t off = 0;
+  for (int i = 0; i < p->d; ++i) {
+    p->dq.N[i] = p->N[i];
+    p->dq.n[i] = p->n[i];
+    p->dq.col[i] = p->cols + off;
+    off += p->N[i];
+  }
+  // factor mode precedence PSI > LUT > DIRECT (transform.py:72-80)
+  int mode = MODE_DIRECT;
+  if (p->f1 & (PRE_PSI | PRE_FULL_PSI)) mode = MODE_TENSOR;
+  else if (p->f1 & PRE_LIN_PSI) mode = MODE_LUT;
+  if (p->psi_policy >= 0 && !(mode == MODE_LUT)) mode = p->psi_policy;
+  if (mode == MODE_LUT || (p->f1 & PRE_LIN_PSI)) {
+    // plan.py:285-295 -- LUT built on the host with the reference's formula
+    std::vector<double> lut((size_t)p->d * (LUT_SIZE + 1));
+    for (int i = 0; i < p->d; ++i) {
+      double h = ((double)p->m / p->n[i]) / LUT_SIZE;
+      for (int t = 0; t <= LUT_SIZE; ++t)
+        lut[(size_t)i * (LUT_SIZE + 1) + t] = host_window(p->window, t * h, p->n[i], p->m, p->b[i]);
+      p->geom.lut_step[i] = LUT_SIZE / ((double)p->m / p->n[i]);
+    }
+    if (!p->lut) NFFTK_CUDA(cudaMalloc(&p->lut, sizeof(double) * lut.size()));
+    NFFTK_CUDA(cudaMemcpyAsync(p->lut, lut.data(), sizeof(double) * lut.size(),
+                               cudaMemcpyHostToDevice, s));
+    p->geom.lut = p->lut;
+  }
+  p->geom.mode = MODE_DIRECT;  // psi table itself is built from exact factors
+  p->geom.psi = nullptr;
+  if (mode == MODE_TENSOR) {
+    size_t count = (size_t)p->M * p->d * (2 * p->m + 1);
+    if (!p->psi) NFFTK_CUDA(cudaMalloc(&p->psi, sizeof(double) * count));
+    build_psi(p->xs, p->M, p->geom, p->psi, s);
+    p->geom.psi = p->psi;
+  }
+  p->geom.mode = mode;
+  p->mode = mode;
+  ensure_grid(p);
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+  p->ready = true;
+}
+
+// ------------------------------------------------------------- transforms
+static void require_ready(const Plan* p) {
+  // transform.py:85-89
+  if (!p->has_nodes) fail(EK_STATE, "plan has no nodes; call set_nodes() first");
+  if (!p->ready) fail(EK_STATE, "plan not precomputed; call precompute() first");
+  if (p->d > MAX_D)
+    fail(EK_SHAPE, "fast transforms support d <= 3, got d=" + std::to_string(p->d));
+}
+
+static void count_evals(Plan* p) {
+  int64_t e = p->mode == MODE_DIRECT ? (int64_t)p->width_sum : 0;
+  p->window_evals_last = e;
+  p->window_evals_total += e;
+}
+
+static void exec_fft(Plan* p, int dir, cudaStream_t s) {
+  NFFTK_CUDA(cudaGetLastError());
+  if (cufftSetStream(p->fft, s) != CUFFT_SUCCESS) fail(EK_CUDA, "cufftSetStream failed");
+  cufftResult r = p->single ? cufftExecC2C(p->fft, (cufftComplex*)p->grid, (cufftComplex*)p->grid, dir)
+                            : cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->grid,
+                                           (cufftDoubleComplex*)p->grid, dir);
+  if (r != CUFFT_SUCCESS) fail(EK_CUDA, "cufftExec failed (" + std::to_string((int)r) + ")");
+}
+
+void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
+  require_ready(p);
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  { PhaseScope ps(p, PH_DECONV, s); launch_deconv(p->single, fhat, p->grid, p->dq, s); }
+  { PhaseScope ps(p, PH_FFT_FWD, s); exec_fft(p, CUFFT_FORWARD, s); }
+  { PhaseScope ps(p, PH_INTERP, s);
+    launch_interp(p->single, p->grid, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+  NFFTK_CUDA(cudaGetLastError());
+  count_evals(p);
+}
+
+void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
+  require_ready(p);
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  { PhaseScope ps(p, PH_ZERO, s);
+    NFFTK_CUDA(cudaMemsetAsync(p->grid, 0, p->elem_bytes() * p->grid_size, s)); }
+  { PhaseScope ps(p, PH_SPREAD, s);
+    launch_spread(p->single, p->grid, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+  NFFTK_CUDA(cudaGetLastError());
+  count_evals(p);
+}
+
+void plan_adjoint_finish_device(Plan* p, void* fhat, cudaStream_t s) {
+  require_ready(p);
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  { PhaseScope ps(p, PH_FFT_INV, s); exec_fft(p, CUFFT_INVERSE, s); }
+  { PhaseScope ps(p, PH_PACK, s); launch_pack(p->single, p->grid, fhat, p->dq, s); }
+  NFFTK_CUDA(cudaGetLastError());
+}
+
+void plan_adjoint_device(Plan* p, const void* f, void* fhat, cudaStream_t s) {
+  plan_spread_device(p, f, s);
+  plan_adjoint_finish_device(p, fhat, s);
+}
+
+static void ensure_io(Plan* p) {
+  if (!p->fhat_dev) NFFTK_CUDA(cudaMalloc(&p->fhat_dev, p->elem_bytes() * p->num_freqs));
+  if (!p->f_dev) NFFTK_CUDA(cudaMalloc(&p->f_dev, p->elem_bytes() * p->M));
+}
+
+void plan_trafo_host(Plan* p, const void* fhat, void* f) {
+  require_ready(p);
+  ensure_stream(p);
+  ensure_io(p);
+  cudaStream_t s = p->own_stream;
+  { PhaseScope ps(p, PH_H2D, s);
+    NFFTK_CUDA(cudaMemcpyAsync(p->fhat_dev, fhat, p->elem_bytes() * p->num_freqs,
+                               cudaMemcpyHostToDevice, s)); }
+  plan_trafo_device(p, p->fhat_dev, p->f_dev, s);
+  { PhaseScope ps(p, PH_D2H, s);
+    NFFTK_CUDA(cudaMemcpyAsync(f, p->f_dev, p->elem_bytes() * p->M, cudaMemcpyDeviceToHost, s)); }
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+}
+
+void plan_adjoint_host(Plan* p, const void* f, void* fhat) {
+  require_ready(p);
+  ensure_stream(p);
+  ensure_io(p);
+  cudaStream_t s = p->own_stream;
+  { PhaseScope ps(p, PH_H2D, s);
+    NFFTK_CUDA(cudaMemcpyAsync(p->f_dev, f, p->elem_bytes() * p->M, cudaMemcpyHostToDevice, s)); }
+  plan_adjoint_device(p, p->f_dev, p->fhat_dev, s);
+  { PhaseScope ps(p, PH_D2H, s);
+    NFFTK_CUDA(cudaMemcpyAsync(fhat, p->fhat_dev, p->elem_bytes() * p->num_freqs,
+                               cudaMemcpyDeviceToHost, s)); }
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+}
+
+void plan_node_order(Plan* p, int64_t* out) {
+  if (!p->has_nodes) fail(EK_STATE, "plan has no nodes; call set_nodes() first");
+  if (p->d > MAX_D) fail(EK_SHAPE, "node order on the device supports d <= 3");
+  ensure_stream(p);
+  int* order = nullptr;
+  NFFTK_CUDA(cudaMalloc(&order, sizeof(int) * p->M));
+  lex_order(p->x_dev, p->M, p->geom, order, p->own_stream);
+  std::vector<int> tmp(p->M);
+  NFFTK_CUDA(cudaMemcpyAsync(tmp.data(), order, sizeof(int) * p->M, cudaMemcpyDeviceToHost,
+                             p->own_stream));
+  NFFTK_CUDA(cudaStreamSynchronize(p->own_stream));
+  cudaFree(order);
+  for (int64_t i = 0; i < p->M; ++i) out[i] = tmp[i];
+}
+
+void plan_bind_grid(Plan* p, void* dev, int64_t bytes) {
+  if (bytes < (int64_t)(p->elem_bytes() * p->grid_size))
+    fail(EK_SHAPE, "grid workspace needs " + std::to_string(p->elem_bytes() * p->grid_size) + " bytes");
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  if (p->grid && !p->grid_external) cudaFree(p->grid);
+  p->grid = dev;
+  p->grid_external = true;
+}
+
+}  // namespace nfftk

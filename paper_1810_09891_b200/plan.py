@@ -1,0 +1,423 @@
+"""Drop-in ``Plan`` of the reference (plan.py:124-327) backed by libnfftk.so.
+
+Same constructor, flag words, defaults, validation order, error classes and
+transform entry points as the reference ``nfftk.Plan``; the work runs on the
+GPU through the C-ABI (include/nfftk.h).  Inputs may be numpy arrays (host
+path: one H2D copy, transform, one D2H copy) or CUDA torch tensors (device
+path: zero-copy, ordered on the current torch stream, returns a tensor).
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import (InvalidFlagError, NfftError, PlanStateError, ShapeError, raise_kind)
+from .indexing import validate_bandlimit
+from .window import WindowModel, kind_code
+
+# Transform flag word f1, reference bit assignment (plan.py:31-43).
+PRE_PHI_HUT = 1 << 0
+FG_PSI = 1 << 1
+PRE_LIN_PSI = 1 << 2
+PRE_FG_PSI = 1 << 3
+PRE_PSI = 1 << 4
+PRE_FULL_PSI = 1 << 5
+MALLOC_X = 1 << 6
+MALLOC_F_HAT = 1 << 7
+MALLOC_F = 1 << 8
+FFT_OUT_OF_PLACE = 1 << 9
+FFTW_INIT = 1 << 10
+NFFT_SORT_NODES = 1 << 11
+NFFT_OMP_BLOCKWISE_ADJOINT = 1 << 12
+_NOOP_F1 = MALLOC_X | MALLOC_F_HAT | MALLOC_F | FFT_OUT_OF_PLACE | FFTW_INIT
+
+# FFT-planner word f2 (plan.py:61-70): accepted and ignored.
+FFTW_MEASURE = 0
+FFTW_DESTROY_INPUT = 1 << 0
+FFTW_UNALIGNED = 1 << 1
+FFTW_CONSERVE_MEMORY = 1 << 2
+FFTW_EXHAUSTIVE = 1 << 3
+FFTW_PRESERVE_INPUT = 1 << 4
+FFTW_PATIENT = 1 << 5
+FFTW_ESTIMATE = 1 << 6
+FFTW_WISDOM_ONLY = 1 << 21
+
+DEFAULT_CUTOFF = 8
+DEFAULT_F2 = FFTW_ESTIMATE | FFTW_DESTROY_INPUT
+LUT_SIZE = 1 << 14
+
+MODE_FOLLOW_FLAGS = -1
+MODE_DIRECT = 0
+MODE_TENSOR = 1
+MODE_LUT = 2
+
+_PRECISIONS = {"double": 0, "complex128": 0, "c128": 0, "single": 1, "complex64": 1, "c64": 1}
+
+
+def default_f1(d):
+    """Default flags (plan.py:77-83): PRE_PHI_HUT | PRE_PSI | sort + no-op bits,
+    plus NFFT_OMP_BLOCKWISE_ADJOINT for d > 1."""
+    flags = PRE_PHI_HUT | PRE_PSI | NFFT_SORT_NODES | _NOOP_F1
+    if d > 1:
+        flags |= NFFT_OMP_BLOCKWISE_ADJOINT
+    return flags
+
+
+def default_n(N):
+    """Componentwise 2 ** (ceil(log2 N_i) + 1) (plan.py:86-92)."""
+    N = validate_bandlimit(N)
+    return tuple(1 << ((v - 1).bit_length() + 1) for v in N)
+
+
+@dataclass
+class PrecomputeTables:
+    """Host view of what precompute built (plan.py:109-121).  The window
+    factor table itself (PRE_PSI) lives on the device in tile-sorted order;
+    ``psi_on_device`` reports it instead of a host array."""
+
+    phi_hut: list = None
+    psi: np.ndarray = None
+    psi_on_device: bool = False
+    lut_on_device: bool = False
+    node_order: np.ndarray = None
+    window_evals: int = 0
+
+
+def _is_torch(a):
+    return type(a).__module__.split(".")[0] == "torch"
+
+
+def _stream_ptr():
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Plan:
+    """Reusable transform plan (reference plan.py:124-327) on a B200."""
+
+    def __init__(self, N, M, n=None, m=None, f1=None, f2=None, window="kaiserbessel",
+                 precision="double"):
+        self._h = 0
+        lib = _lib.load()
+        self.N = validate_bandlimit(N)
+        self.d = len(self.N)
+        self.M = int(M)
+        nvec = None
+        if n is not None:
+            try:
+                nvec = tuple(int(v) for v in n)
+            except TypeError:
+                nvec = (int(n),)
+            if len(nvec) != self.d:
+                raise ShapeError(f"n has {len(nvec)} dims, N has {self.d}")
+        if f1 is not None:
+            f1 = int(f1)
+            if f1 < 0 or f1 != f1 & 0xFFFFFFFF:
+                raise InvalidFlagError(f"f1 must be an unsigned 32-bit word, got {f1}")
+        prec = _PRECISIONS.get(str(precision).lower())
+        if prec is None:
+            raise NfftError(f"unknown precision {precision!r}; use 'double' or 'single'")
+        try:
+            code = kind_code(window)
+            bad_window = None
+        except NfftError as exc:  # reported after the other checks, as in plan.py:179
+            code, bad_window = 0, exc
+        h = lib.nfftk_create_ex(
+            _lib.i32_array(self.N), self.d, max(-(1 << 31), min(self.M, (1 << 31) - 1)),
+            _lib.i32_array(nvec) if nvec is not None else None,
+            int(m is not None), int(m) if m is not None else 0,
+            int(f1 is not None), (f1 or 0) & 0xFFFFFFFF,
+            int(f2 is not None), (int(f2) & 0xFFFFFFFF) if f2 is not None else 0,
+            code, prec)
+        if h < 0:
+            raise_kind(lib.nfftk_last_create_error_kind(),
+                       lib.nfftk_last_create_error_message().decode())
+        self._h = h
+        if bad_window is not None:
+            self.close()
+            raise bad_window
+        self._lib = lib
+        self.single = prec == 1
+        self.precision = "single" if self.single else "double"
+        p = self._params()
+        self.m = int(p[2])
+        self.f1 = int(p[5])
+        self.f2 = int(p[6])
+        nn = (ctypes.c_int32 * self.d)()
+        tt = (ctypes.c_int32 * self.d)()
+        lib.nfftk_get_sizes(h, None, nn, tt, self.d)
+        self.n = tuple(int(v) for v in nn)
+        self.tile = tuple(int(v) for v in tt)
+        self.window = WindowModel.make(window, self.N, self.n, self.m)
+        self._x = None
+        self._node_order = None
+        self._order_valid = False
+
+    # -- plumbing -------------------------------------------------------
+    def _params(self):
+        out = (ctypes.c_int64 * 13)()
+        self._lib_checked().nfftk_get_params(self._h, out, 13)
+        return list(out)
+
+    def _lib_checked(self):
+        if not self._h:
+            raise PlanStateError("plan is closed")
+        return _lib.load()
+
+    def _check(self, rc):
+        if rc != 0:
+            lib = self._lib
+            raise_kind(lib.nfftk_last_error_kind(self._h),
+                       lib.nfftk_last_error_message(self._h).decode())
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def cdtype(self):
+        return np.complex64 if self.single else np.complex128
+
+    def close(self):
+        if self._h:
+            _lib.load().nfftk_destroy(self._h)
+            self._h = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- sizes ------------------------------------------------------------
+    @property
+    def num_freqs(self):
+        return math.prod(self.N)
+
+    @property
+    def grid_size(self):
+        return math.prod(self.n)
+
+    # -- nodes (plan.py:202-237) -----------------------------------------
+    @property
+    def x(self):
+        return self._x
+
+    @x.setter
+    def x(self, coords):
+        self.set_nodes(coords)
+
+    def set_nodes(self, coords):
+        """Store the node set (strict [-1/2, 1/2) check, no folding); sorts the
+        nodes into grid tiles on the device.  Invalidates precomputed tables."""
+        lib = self._lib_checked()
+        if _is_torch(coords) and coords.is_cuda:
+            import torch
+
+            if tuple(coords.shape) != (self.M, self.d):
+                raise ShapeError(f"nodes must have shape {(self.M, self.d)}, got {tuple(coords.shape)}")
+            coords = coords.to(torch.float64).contiguous()
+            self._check(lib.nfftk_set_nodes_device(self._h, ctypes.c_void_p(coords.data_ptr()),
+                                                   coords.numel(), _stream_ptr()))
+        else:
+            coords = np.asarray(coords, dtype=np.float64)
+            if coords.shape != (self.M, self.d):
+                raise ShapeError(f"nodes must have shape {(self.M, self.d)}, got {coords.shape}")
+            coords = np.ascontiguousarray(coords)
+            self._check(lib.nfftk_set_nodes(self._h, coords.ctypes.data, coords.size))
+        self._x = coords
+        self._order_valid = False
+
+    @property
+    def node_order(self):
+        """Lexicographic cell order of the nodes when NFFT_SORT_NODES is set
+        (plan.py:228-233), computed by a stable device radix sort."""
+        if not (self.f1 & NFFT_SORT_NODES) or self._x is None:
+            return None
+        if not self._order_valid:
+            out = np.empty(self.M, dtype=np.int64)
+            self._check(self._lib.nfftk_node_order(
+                self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), self.M))
+            self._node_order = out
+            self._order_valid = True
+        return self._node_order
+
+    # -- precompute (plan.py:241-299) ------------------------------------
+    @property
+    def ready(self):
+        return bool(self._params()[8])
+
+    def set_psi_policy(self, mode):
+        """Extension: force the window-factor source (MODE_DIRECT / MODE_TENSOR)
+        regardless of f1; results are identical (kernels.py modes agree)."""
+        self._check(self._lib_checked().nfftk_set_psi_policy(self._h, int(mode)))
+
+    def precompute(self):
+        lib = self._lib_checked()
+        if self._x is not None and _is_torch(self._x):
+            self._check(lib.nfftk_precompute_stream(self._h, _stream_ptr()))
+        else:
+            self._check(lib.nfftk_precompute(self._h))
+        return self.tables
+
+    @property
+    def tables(self):
+        p = self._params()
+        if not p[8]:
+            return None
+        t = PrecomputeTables()
+        if self.f1 & PRE_PHI_HUT:
+            t.phi_hut = [self.phi_hut(i) for i in range(self.d)]
+        t.psi_on_device = p[9] == MODE_TENSOR
+        t.lut_on_device = bool(self.f1 & PRE_LIN_PSI)
+        evals = 0
+        if self.f1 & (PRE_PSI | PRE_FULL_PSI):
+            evals += int(p[12])
+        if self.f1 & PRE_LIN_PSI:
+            evals += self.d * (LUT_SIZE + 1)
+        t.window_evals = evals
+        t.node_order = self.node_order
+        return t
+
+    def phi_hut(self, i):
+        out = np.empty(self.N[i] + 1)
+        self._check(self._lib_checked().nfftk_phi_hut(
+            self._h, int(i), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size))
+        return out
+
+    @property
+    def mode(self):
+        return int(self._params()[9])
+
+    @property
+    def window_evals_last(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._lib_checked().nfftk_window_evals(self._h, ctypes.byref(a), ctypes.byref(b))
+        return a.value
+
+    @property
+    def window_evals_total(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._lib_checked().nfftk_window_evals(self._h, ctypes.byref(a), ctypes.byref(b))
+        return b.value
+
+    # -- transforms (transform.py:92-176) ---------------------------------
+    def _require_ready(self):
+        p = self._params()
+        if not p[7]:
+            raise PlanStateError("plan has no nodes; call set_nodes() first")
+        if not p[8]:
+            raise PlanStateError("plan not precomputed; call precompute() first")
+
+    def _as_vector(self, arr, length, what):
+        out = np.asarray(arr)
+        if out.shape == (length,):
+            pass
+        elif out.ndim >= 1 and out.size == length:
+            out = out.reshape(length)
+        else:
+            raise ShapeError(f"{what} must have {length} entries, got shape {out.shape}")
+        return np.ascontiguousarray(out, dtype=self.cdtype)
+
+    def _as_tensor(self, t, length, what):
+        import torch
+
+        if t.numel() != length or t.dim() < 1:
+            raise ShapeError(f"{what} must have {length} entries, got shape {tuple(t.shape)}")
+        want = torch.complex64 if self.single else torch.complex128
+        return t.reshape(length).to(want).contiguous()
+
+    def trafo(self, fhat, out=None):
+        """f = B F D f_hat at the M nodes (transform.py:92-118)."""
+        lib = self._lib_checked()
+        self._require_ready()
+        if _is_torch(fhat) and fhat.is_cuda:
+            import torch
+
+            fhat = self._as_tensor(fhat, self.num_freqs, "fhat")
+            if out is None:
+                out = torch.empty(self.M, dtype=fhat.dtype, device=fhat.device)
+            self._check(lib.nfftk_trafo_device(self._h, ctypes.c_void_p(fhat.data_ptr()),
+                                               ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
+            return out
+        fhat = self._as_vector(fhat, self.num_freqs, "fhat")
+        if out is None:
+            out = np.empty(self.M, dtype=self.cdtype)
+        self._check(lib.nfftk_trafo_host(self._h, fhat.ctypes.data, out.ctypes.data))
+        return out
+
+    def adjoint(self, f, out=None):
+        """f_hat = D^H F^H B^H f (transform.py:121-176)."""
+        lib = self._lib_checked()
+        self._require_ready()
+        if _is_torch(f) and f.is_cuda:
+            import torch
+
+            f = self._as_tensor(f, self.M, "f")
+            if out is None:
+                out = torch.empty(self.num_freqs, dtype=f.dtype, device=f.device)
+            self._check(lib.nfftk_adjoint_device(self._h, ctypes.c_void_p(f.data_ptr()),
+                                                 ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
+            return out
+        f = self._as_vector(f, self.M, "f")
+        if out is None:
+            out = np.empty(self.num_freqs, dtype=self.cdtype)
+        self._check(lib.nfftk_adjoint_host(self._h, f.ctypes.data, out.ctypes.data))
+        return out
+
+    # -- multi-GPU building blocks (distributed.py) -----------------------
+    def spread(self, f):
+        """B^H only, into the plan grid (device tensor input)."""
+        f = self._as_tensor(f, self.M, "f")
+        self._check(self._lib_checked().nfftk_spread_device(
+            self._h, ctypes.c_void_p(f.data_ptr()), _stream_ptr()))
+
+    def adjoint_finish(self, out):
+        """F^H and D^H of the (already reduced) plan grid into ``out``."""
+        self._check(self._lib_checked().nfftk_adjoint_finish_device(
+            self._h, ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
+        return out
+
+    def bind_grid(self, tensor):
+        """Use a caller-owned device tensor as the plan's oversampled grid."""
+        nbytes = tensor.numel() * tensor.element_size()
+        self._check(self._lib_checked().nfftk_bind_grid(self._h, ctypes.c_void_p(tensor.data_ptr()),
+                                                        nbytes))
+        self._bound_grid = tensor
+
+    # -- instrumentation ------------------------------------------------
+    def set_timing(self, on=True):
+        self._lib_checked().nfftk_set_timing(self._h, int(bool(on)))
+
+    def phase_times(self, reset=False):
+        """Accumulated CUDA-event milliseconds and call counts per phase."""
+        n = len(_lib.PHASES)
+        ms = (ctypes.c_double * n)()
+        calls = (ctypes.c_int64 * n)()
+        self._check(self._lib_checked().nfftk_phase_times(self._h, ms, calls, n, int(bool(reset))))
+        return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.PHASES)}
+
+    def ndft(self, fhat):
+        raise NotImplementedError("exact NDFT is a test oracle (oracle/), not part of the GPU library")
+
+    def ndft_adjoint(self, f):
+        raise NotImplementedError("exact NDFT is a test oracle (oracle/), not part of the GPU library")
+
+    def __repr__(self):
+        return (f"Plan(N={self.N}, M={self.M}, n={self.n}, m={self.m}, "
+                f"f1={hex(self.f1)}, f2={hex(self.f2)}, window={self.window.kind!r})")
+
+
+def launch_count():
+    """Kernels launched by libnfftk.so in this process."""
+    return int(_lib.load().nfftk_launch_count())
