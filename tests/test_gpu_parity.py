@@ -1,0 +1,359 @@
+"""GPU parity tests: the CUDA path (through the C-ABI library) against the
+CPU oracle (oracle/, pinned to the live reference) and the committed golden
+vectors of the reference itself.
+
+Tolerances (BASELINE.json north_star): relative l2 <= 1e-12 for complex128,
+<= 1e-5 for complex64 (the reference has no complex64 path; its complex128
+output is the oracle).  NDFT bands are m-aware.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+import paper_1810_09891_b200 as nf
+from paper_1810_09891_b200 import _lib
+from paper_1810_09891_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+TOL128 = 1e-12
+TOL64 = 1e-5
+
+SMALL = np.load(os.path.join(GOLDEN, "small_cases.npz"))
+NAMES = sorted({k.split("__")[0] for k in SMALL.files})
+
+
+def case(name):
+    return {f: SMALL[f"{name}__{f}"] for f in
+            ("N", "n", "m", "x", "fhat", "f", "trafo", "adjoint", "order", "f1", "window",
+             "ndft", "ndft_adjoint")}
+
+
+def e2(ref, got):
+    ref = np.asarray(ref).astype(np.complex128).ravel()
+    got = np.asarray(got).astype(np.complex128).ravel()
+    return float(np.linalg.norm(ref - got) / np.linalg.norm(ref))
+
+
+def make_plan(c, precision="double", psi=None):
+    p = nf.Plan(tuple(c["N"]), c["x"].shape[0], n=tuple(c["n"]), m=int(c["m"]),
+                f1=int(c["f1"]), window=str(c["window"]), precision=precision)
+    if psi is not None:
+        p.set_psi_policy(psi)
+    p.x = c["x"]
+    p.precompute()
+    return p
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    assert t.cuda.is_available(), "GPU tests need a CUDA device"
+    return t
+
+
+# ------------------------------------------------------------ golden cases
+@pytest.mark.parametrize("name", NAMES)
+def test_small_cases_vs_reference_goldens(name):
+    c = case(name)
+    p = make_plan(c)
+    assert e2(c["trafo"], p.trafo(c["fhat"])) < TOL128
+    assert e2(c["adjoint"], p.adjoint(c["f"])) < TOL128
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_small_cases_vs_oracle(name, oracle):
+    c = case(name)
+    lut = bool(int(c["f1"]) & nf.PRE_LIN_PSI) and not (int(c["f1"]) & (nf.PRE_PSI | nf.PRE_FULL_PSI))
+    p = make_plan(c)
+    ref_f = oracle.trafo(c["N"], c["n"], int(c["m"]), c["x"], c["fhat"], window=str(c["window"]), lut=lut)
+    ref_a = oracle.adjoint(c["N"], c["n"], int(c["m"]), c["x"], c["f"], window=str(c["window"]), lut=lut)
+    assert e2(ref_f, p.trafo(c["fhat"])) < TOL128
+    assert e2(ref_a, p.adjoint(c["f"])) < TOL128
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if int(case(n)["m"]) >= 6 and "lut" not in n])
+def test_small_cases_vs_ndft(name):
+    """Exact-sum check: the fast transform is within its own truncation error
+    of the NDFT (reference E2 for the same inputs, 10x band)."""
+    c = case(name)
+    p = make_plan(c)
+    band_f = max(10 * e2(c["ndft"], c["trafo"]), 1e-14)
+    band_a = max(10 * e2(c["ndft_adjoint"], c["adjoint"]), 1e-14)
+    assert e2(c["ndft"], p.trafo(c["fhat"])) < band_f
+    assert e2(c["ndft_adjoint"], p.adjoint(c["f"])) < band_a
+
+
+def test_table4_accuracy_d1_m8():
+    """SPEC acceptance: E2 vs NDFT <= 1e-13 at m = 8 (Table 4 style)."""
+    c = case("d1_m8")
+    p = make_plan(c)
+    assert e2(c["ndft"], p.trafo(c["fhat"])) < 1e-13
+    assert e2(c["ndft_adjoint"], p.adjoint(c["f"])) < 1e-13
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_config_goldens_full(cfg):
+    w = wl.CONFIGS[cfg]
+    g = np.load(os.path.join(GOLDEN, f"{cfg}.npz"))
+    p = nf.Plan(w.N, w.M, n=w.n, m=w.m)
+    p.x = wl.nodes(w)
+    p.precompute()
+    assert e2(g["trafo"], p.trafo(wl.fhat(w))) < TOL128
+    assert e2(g["adjoint"], p.adjoint(wl.samples(w))) < TOL128
+
+
+def test_config_c3_golden_and_oracle(oracle):
+    w = wl.CONFIGS["C3"]
+    g = np.load(os.path.join(GOLDEN, "C3.npz"))
+    x, fh, fs = wl.nodes(w), wl.fhat(w), wl.samples(w)
+    p = nf.Plan(w.N, w.M, n=w.n, m=w.m)
+    p.x = x
+    p.precompute()
+    f = p.trafo(fh)
+    a = p.adjoint(fs)
+    assert e2(g["trafo_sub"], f[g["trafo_idx"]]) < TOL128
+    assert e2(g["adjoint_sub"], a[g["adjoint_idx"]]) < TOL128
+    assert e2(oracle.trafo(w.N, w.n, w.m, x, fh), f) < TOL128
+    assert e2(oracle.adjoint(w.N, w.n, w.m, x, fs), a) < TOL128
+
+
+# ------------------------------------------------------------ complex64
+@pytest.mark.parametrize("name", ["d1_m8", "d2_m8", "d2_clustered", "d3_m6", "d3_aligned", "d2_gauss"])
+def test_complex64_vs_c128_reference(name):
+    c = case(name)
+    p = make_plan(c, precision="single")
+    assert e2(c["trafo"], p.trafo(c["fhat"])) < TOL64
+    assert e2(c["adjoint"], p.adjoint(c["f"])) < TOL64
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_complex64_configs(cfg, oracle):
+    w = wl.CONFIGS[cfg]
+    x, fh, fs = wl.nodes(w), wl.fhat(w), wl.samples(w)
+    p = nf.Plan(w.N, w.M, n=w.n, m=w.m, precision="single")
+    p.x = x
+    p.precompute()
+    assert e2(oracle.trafo(w.N, w.n, w.m, x, fh), p.trafo(fh)) < TOL64
+    assert e2(oracle.adjoint(w.N, w.n, w.m, x, fs), p.adjoint(fs)) < TOL64
+
+
+# ------------------------------------------------- modes / paths agree
+def test_direct_and_tensor_modes_agree():
+    """kernels.py modes DIRECT and TENSOR use identical factors (SPEC: <= 1e-14)."""
+    c = case("d3_m6")
+    a = make_plan(c, psi=nf.MODE_DIRECT)
+    b = make_plan(c, psi=nf.MODE_TENSOR)
+    assert a.mode == nf.MODE_DIRECT and b.mode == nf.MODE_TENSOR
+    assert np.array_equal(a.trafo(c["fhat"]), b.trafo(c["fhat"]))
+    assert e2(a.adjoint(c["f"]), b.adjoint(c["f"])) < 1e-14
+
+
+def test_full_psi_flag_maps_to_tensor():
+    c = dict(case("d2_small"))
+    c["f1"] = np.array(nf.PRE_PHI_HUT | nf.PRE_FULL_PSI)
+    p = make_plan(c)
+    assert p.mode == nf.MODE_TENSOR
+    assert e2(c["trafo"], p.trafo(c["fhat"])) < TOL128
+
+
+def test_lut_mode_tolerance_vs_exact():
+    """PRE_LIN_PSI stays within the documented 1e-6 of the exact window (SPEC)."""
+    c = case("d3_lut")
+    exact = dict(c)
+    exact["f1"] = np.array(nf.PRE_PHI_HUT | nf.PRE_PSI)
+    assert e2(make_plan(exact).trafo(c["fhat"]), make_plan(c).trafo(c["fhat"])) < 1e-6
+
+
+def test_device_path_equals_host_path(torch):
+    c = case("d2_m8")
+    p = make_plan(c)
+    fh_host = p.trafo(c["fhat"])
+    fh_dev = p.trafo(torch.from_numpy(c["fhat"]).cuda()).cpu().numpy()
+    assert np.array_equal(fh_host, fh_dev)
+    q = nf.Plan(tuple(c["N"]), c["x"].shape[0], n=tuple(c["n"]), m=int(c["m"]))
+    q.x = torch.from_numpy(c["x"]).cuda()
+    q.precompute()
+    assert np.array_equal(q.trafo(c["fhat"]), fh_host)
+
+
+def test_trafo_deterministic_adjoint_stable():
+    c = case("d3_m6")
+    p = make_plan(c)
+    assert np.array_equal(p.trafo(c["fhat"]), p.trafo(c["fhat"]))
+    assert e2(p.adjoint(c["f"]), p.adjoint(c["f"])) < 1e-15
+
+
+# -------------------------------------------------------------- C-ABI
+def test_abi_spec_example():
+    """SPEC cabi example: N=(4), M=1, x=0, f_hat_0 = 1 -> f = 1 within 1e-13."""
+    lib = _lib.load()
+    h = lib.nfftk_create(_lib.i32_array([4]), 1, 1)
+    assert h > 0
+    x = np.array([0.0])
+    assert lib.nfftk_set_x(h, x.ctypes.data, 1) == 0, lib.nfftk_last_error_message(h)
+    fh = np.array([0, 0, 0, 0, 1, 0, 0, 0], dtype=np.float64)
+    assert lib.nfftk_set_fhat(h, fh.ctypes.data, 8) == 0
+    assert lib.nfftk_trafo(h) == 0
+    f = np.ctypeslib.as_array(ctypes.cast(lib.nfftk_get_f(h), ctypes.POINTER(ctypes.c_double)), (2,))
+    assert abs(f[0] - 1.0) < 1e-13 and abs(f[1]) < 1e-13
+    assert lib.nfftk_destroy(h) == 0
+
+
+def test_abi_matches_python_api_bitwise():
+    c = case("d3_m6")
+    lib = _lib.load()
+    d = int(c["x"].shape[1])
+    h = lib.nfftk_create_advanced(_lib.i32_array(c["N"]), d, c["x"].shape[0],
+                                  _lib.i32_array(c["n"]), int(c["m"]), int(c["f1"]), 0x41)
+    assert h > 0
+    x = np.ascontiguousarray(c["x"])
+    assert lib.nfftk_set_x(h, x.ctypes.data, x.size) == 0
+    fh = np.ascontiguousarray(c["fhat"]).view(np.float64)
+    assert lib.nfftk_set_fhat(h, fh.ctypes.data, fh.size) == 0
+    assert lib.nfftk_trafo(h) == 0
+    M = x.shape[0]
+    f = np.ctypeslib.as_array(ctypes.cast(lib.nfftk_get_f(h), ctypes.POINTER(ctypes.c_double)),
+                              (2 * M,)).view(np.complex128)
+    p = make_plan(c)
+    assert np.array_equal(f, p.trafo(c["fhat"]))
+    fs = np.ascontiguousarray(c["f"]).view(np.float64)
+    assert lib.nfftk_set_f(h, fs.ctypes.data, fs.size) == 0
+    assert lib.nfftk_adjoint(h) == 0
+    K = int(np.prod(c["N"]))
+    a = np.ctypeslib.as_array(ctypes.cast(lib.nfftk_get_fhat(h), ctypes.POINTER(ctypes.c_double)),
+                              (2 * K,)).view(np.complex128)
+    assert e2(c["adjoint"], a) < TOL128
+    assert lib.nfftk_destroy(h) == 0
+
+
+def test_abi_rank4_quirks():
+    """Reference quirks: rank-4 set_x succeeds, trafo -> -2;
+    rank-4 with PRE_FULL_PSI -> set_x -9."""
+    lib = _lib.load()
+    N = _lib.i32_array([4, 4, 4, 4])
+    n = _lib.i32_array([8, 8, 8, 8])
+    x = np.zeros(8)
+    h = lib.nfftk_create_advanced(N, 4, 2, n, 2, 0x1fd1, 0x41)
+    assert lib.nfftk_set_x(h, x.ctypes.data, 8) == 0
+    assert lib.nfftk_trafo(h) == -2
+    assert lib.nfftk_last_error_message(h) == b"fast transforms support d <= 3, got d=4"
+    lib.nfftk_destroy(h)
+    h = lib.nfftk_create_advanced(N, 4, 2, n, 2, 0x1fd1 | nf.PRE_FULL_PSI, 0x41)
+    assert lib.nfftk_set_x(h, x.ctypes.data, 8) == -9
+    lib.nfftk_destroy(h)
+
+
+def test_state_errors():
+    p = nf.Plan((16,), 4, n=(32,), m=4)
+    with pytest.raises(nf.PlanStateError, match="no nodes"):
+        p.trafo(np.zeros(16))
+    p.set_nodes(np.zeros((4, 1)))
+    with pytest.raises(nf.PlanStateError, match="not precomputed"):
+        p.trafo(np.zeros(16))
+    p.precompute()
+    with pytest.raises(nf.ShapeError):
+        p.trafo(np.zeros(15))
+    assert p.trafo(np.zeros((4, 4))).shape == (4,)
+
+
+# -------------------------------------------------------- properties
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_adjoint_identity(d):
+    """SPEC: |<A fh, f> - <fh, A^H f>| / (|fh| |f|) <= 1e-12 over random instances."""
+    rng = np.random.default_rng(100 + d)
+    for _ in range(10):
+        N = tuple(int(v) for v in 2 * rng.integers(2, 9, d))
+        n = tuple(2 * v for v in N)
+        m = int(rng.integers(1, min(n) // 2))
+        m = max(1, min(m, (min(n) - 1) // 2, 8))
+        M = int(rng.integers(1, 300))
+        p = nf.Plan(N, M, n=n, m=m)
+        p.x = rng.random((M, d)) - 0.5
+        p.precompute()
+        K = int(np.prod(N))
+        fh = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+        f = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+        lhs = np.vdot(f, p.trafo(fh))
+        rhs = np.vdot(p.adjoint(f), fh)
+        assert abs(lhs - rhs) / (np.linalg.norm(fh) * np.linalg.norm(f)) < 1e-12
+
+
+def test_node_order_matches_lexsort(oracle):
+    for name in ("d2_aligned", "d3_aniso", "d2_clustered"):
+        c = case(name)
+        p = make_plan(c)
+        assert np.array_equal(p.node_order, c["order"])
+
+
+def test_window_eval_counter():
+    c = dict(case("d2_aligned"))
+    c["f1"] = np.array(nf.PRE_PHI_HUT)  # DIRECT mode: counts evaluations
+    p = make_plan(c)
+    p.trafo(c["fhat"])
+    lo, width = nf.indexing.node_ranges(c["x"], tuple(c["n"]), int(c["m"]))
+    assert p.window_evals_last == int(width.sum())
+    p.adjoint(c["f"])
+    assert p.window_evals_total == 2 * int(width.sum())
+    assert p.window_evals_total <= 2 * (2 * int(c["m"]) + 1) ** 2 * c["x"].shape[0] * 2
+
+
+def test_tiny_grid_halo_wraps(oracle):
+    """Halo larger than the grid (T + 2m + 1 > n): cells alias onto themselves."""
+    rng = np.random.default_rng(3)
+    for N, n, m in [((4,), (8,), 3), ((4, 4), (8, 10), 3), ((2, 2, 2), (8, 8, 8), 3)]:
+        M = 57
+        x = rng.random((M, len(N))) - 0.5
+        x[0] = -0.5
+        K = int(np.prod(N))
+        fh = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+        fs = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+        p = nf.Plan(N, M, n=n, m=m)
+        p.x = x
+        p.precompute()
+        assert e2(oracle.trafo(N, n, m, x, fh), p.trafo(fh)) < TOL128
+        assert e2(oracle.adjoint(N, n, m, x, fs), p.adjoint(fs)) < TOL128
+
+
+def test_dense_single_cell_nodes(oracle):
+    """Many nodes in one cell (heavy subproblem splitting + contention)."""
+    rng = np.random.default_rng(4)
+    N, n, m, M = (32, 32), (64, 64), 6, 5000
+    x = 0.01 + 1e-4 * rng.random((M, 2))
+    fh = rng.standard_normal(1024) + 1j * rng.standard_normal(1024)
+    fs = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    p = nf.Plan(N, M, n=n, m=m)
+    p.x = x
+    p.precompute()
+    assert e2(oracle.trafo(N, n, m, x, fh), p.trafo(fh)) < TOL128
+    assert e2(oracle.adjoint(N, n, m, x, fs), p.adjoint(fs)) < TOL128
+
+
+# ------------------------------------------------- full-size properties
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_full_size_trafo_subsample_and_adjoint_identity(cfg, oracle, torch):
+    """At BASELINE sizes: trafo on a node subsample equals the oracle run on
+    those nodes (trafo is per-node independent), and the adjoint satisfies
+    the adjoint identity against the trafo at full size."""
+    w = wl.CONFIGS[cfg]
+    x = wl.nodes(w)
+    fh = wl.fhat(w)
+    p = nf.Plan(w.N, w.M, n=w.n, m=w.m)
+    p.x = torch.from_numpy(x).cuda()
+    p.precompute()
+    fh_d = torch.from_numpy(fh).cuda()
+    f = p.trafo(fh_d)
+    idx = np.sort(np.random.default_rng(9).choice(w.M, 512, replace=False))
+    ref = oracle.trafo(w.N, w.n, w.m, x[idx], fh)
+    assert e2(ref, f[torch.from_numpy(idx).cuda()].cpu().numpy()) < TOL128
+    g = torch.from_numpy(wl.samples(w)).cuda()
+    a = p.adjoint(g)
+    lhs = torch.vdot(g, f).item()
+    rhs = torch.vdot(a, fh_d).item()
+    scale = torch.linalg.norm(fh_d).item() * torch.linalg.norm(g).item()
+    assert abs(lhs - rhs) / scale < 1e-12
