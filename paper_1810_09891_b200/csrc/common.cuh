@@ -118,6 +118,7 @@ struct Geom {
   double lut_step[MAX_D];
   const double* psi;      // M * d * (2m+1) in sorted order (MODE_TENSOR)
   int64_t M;
+  int nt_interp;          // threads per interp CTA
 };
 
 // -------------------------------------------------------- device window

@@ -16,7 +16,7 @@ namespace nfftk {
 
 static unsigned long long g_launches = 0;  // kernels launched by this library
 unsigned long long launch_count() { return g_launches; }
-static inline void count_launch() { ++g_launches; }
+void count_launch() { ++g_launches; }
 
 static inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148LL * 64) {
   int64_t b = (work + threads - 1) / threads;
@@ -340,366 +340,6 @@ void launch_pack_deconv(const void* grid, void* fhat, const DeconvGeom& q, cudaS
   count_launch();
 }
 
-// ---------------------------------------------------- tile halo helpers
-template <int D>
-__device__ __forceinline__ void tile_origin(const Geom& g, int tile, int* tc, int* org) {
-  int t = tile;
-#pragma unroll
-  for (int i = D - 1; i >= 0; --i) {
-    tc[i] = t % g.ntile[i];
-    t /= g.ntile[i];
-  }
-#pragma unroll
-  for (int i = 0; i < D; ++i) org[i] = tc[i] * g.T[i] - g.m;
-}
-
-// linear grid slot of halo cell idx (halo row-major, last dim fastest)
-template <int D>
-__device__ __forceinline__ int64_t halo_slot(const Geom& g, const int* org, int idx) {
-  int a[D];
-  int rem = idx;
-#pragma unroll
-  for (int i = D - 1; i >= 0; --i) {
-    a[i] = rem % g.H[i];
-    rem /= g.H[i];
-  }
-  int64_t lin = 0;
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    int s = org[i] + a[i];
-    s = s % g.n[i];
-    if (s < 0) s += g.n[i];
-    lin = lin * g.n[i] + s;
-  }
-  return lin;
-}
-
-// Per-node stencil in halo coordinates: h = (cell slot - tile start) + m -
-// (cell - lo); with cell - lo in {m-1, m} this stays inside [0, T + 2m].
-template <int D>
-__device__ __forceinline__ void node_stencil(const Geom& g, const int* tc, const double* x,
-                                             int* h, int* W, int64_t* lo) {
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    Stencil st = stencil(x[i], g.nd[i], g.md);
-    int64_t slot = floor_mod(st.cell, g.n[i]);
-    h[i] = (int)(slot - (int64_t)tc[i] * g.T[i]) + g.m - (int)(st.cell - st.lo);
-    W[i] = st.width;
-    lo[i] = st.lo;
-  }
-}
-
-template <typename R, int D>
-__device__ __forceinline__ void node_weights(const Geom& g, int64_t i, const double* x,
-                                             const int64_t* lo, const int* W, R* wb, int lane,
-                                             int nlanes) {
-  const int K = 2 * g.m + 1;
-  for (int q = lane; q < D * K; q += nlanes) {
-    int dim = q / K, t = q - dim * K;
-    R v = 0;
-    if (t < W[dim]) {
-      if (g.mode == MODE_TENSOR)
-        v = (R)g.psi[(i * D + dim) * K + t];
-      else
-        v = (R)(dim_factor(g, dim, x[dim], lo[dim] + t) * g.wscale[dim]);
-    }
-    wb[q] = v;
-  }
-}
-
-__device__ __forceinline__ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-
-// ---------------------------------------------------------------- B (interp)
-// kernels.py:122-197.  One CTA per subproblem (<= maxsub nodes of one tile):
-// the tile's (T+2m+1)^d halo is staged in shared memory, then each warp takes
-// one node at a time; lanes split the leading stencil dims and run along the
-// contiguous last dim; a warp-shuffle reduction forms f_j.
-template <typename R, int D>
-__global__ void __launch_bounds__(256)
-k_interp_tiled(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
-               const double* __restrict__ xs, const int* __restrict__ perm,
-               const int4* __restrict__ subs, Geom g) {
-  using C = cplx_t<R>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = 2 * g.m + 1;
-  int hsz = 1;
-#pragma unroll
-  for (int i = 0; i < D; ++i) hsz *= g.H[i];
-  C* halo = reinterpret_cast<C*>(smem_raw);
-  R* wbuf = reinterpret_cast<R*>(smem_raw + align16((size_t)hsz * sizeof(C)));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  R* wmy = wbuf + warp * D * K;
-  const int4 sp = subs[blockIdx.x];
-  int tc[D], org[D];
-  tile_origin<D>(g, sp.x, tc, org);
-  for (int idx = threadIdx.x; idx < hsz; idx += blockDim.x) halo[idx] = grid[halo_slot<D>(g, org, idx)];
-  __syncthreads();
-
-  const int H1 = D > 1 ? g.H[1] : 1;
-  const int H2 = D > 2 ? g.H[2] : 1;
-  for (int i = sp.y + warp; i < sp.y + sp.z; i += nwarps) {
-    double x[D];
-#pragma unroll
-    for (int dd = 0; dd < D; ++dd) x[dd] = xs[dd * g.M + i];
-    int h[D], W[D];
-    int64_t lo[D];
-    node_stencil<D>(g, tc, x, h, W, lo);
-    node_weights<R, D>(g, i, x, lo, W, wmy, lane, 32);
-    __syncwarp();
-    R are = 0, aim = 0;
-    if constexpr (D == 1) {
-      for (int t0 = lane; t0 < W[0]; t0 += 32) {
-        C v = halo[h[0] + t0];
-        R w = wmy[t0];
-        are += w * v.x;
-        aim += w * v.y;
-      }
-    } else if constexpr (D == 2) {
-      for (int t0 = lane; t0 < W[0]; t0 += 32) {
-        const C* row = halo + (h[0] + t0) * H1 + h[1];
-        R sre = 0, sim = 0;
-        for (int t1 = 0; t1 < W[D - 1]; ++t1) {
-          C v = row[t1];
-          R w = wmy[K + t1];
-          sre += w * v.x;
-          sim += w * v.y;
-        }
-        R w0 = wmy[t0];
-        are += w0 * sre;
-        aim += w0 * sim;
-      }
-    } else {
-      const int P = W[0] * W[1];
-      for (int p = lane; p < P; p += 32) {
-        int t0 = p / W[1], t1 = p - t0 * W[1];
-        const C* row = halo + ((h[0] + t0) * H1 + h[1] + t1) * H2 + h[D - 1];
-        R sre = 0, sim = 0;
-        for (int t2 = 0; t2 < W[D - 1]; ++t2) {
-          C v = row[t2];
-          R w = wmy[2 * K + t2];
-          sre += w * v.x;
-          sim += w * v.y;
-        }
-        R w01 = wmy[t0] * wmy[K + t1];
-        are += w01 * sre;
-        aim += w01 * sim;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      are += __shfl_xor_sync(0xffffffffu, are, off);
-      aim += __shfl_xor_sync(0xffffffffu, aim, off);
-    }
-    if (lane == 0) {
-      C v;
-      v.x = are;
-      v.y = aim;
-      fout[perm[i]] = v;
-    }
-    __syncwarp();
-  }
-}
-
-// -------------------------------------------------------------- B^H (spread)
-// kernels.py:209-401.  One CTA per subproblem accumulates into a shared-memory
-// halo without atomics: halo rows along dim 0 are owned round-robin by "row
-// units" (d=3: warps, d=2: half-warps, d=1: threads), so two units never touch
-// the same cell -- the GPU analogue of the reference's slab ownership
-// (kernels.py:13-17).  Node weights are computed once per batch and shared.
-// The finished halo is added to the HBM grid with fp64 RED atomics.
-constexpr int SPREAD_BATCH = 32;
-
-template <typename R, int D>
-__global__ void __launch_bounds__(256)
-k_spread_tiled(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fin,
-               const double* __restrict__ xs, const int* __restrict__ perm,
-               const int4* __restrict__ subs, Geom g) {
-  using C = cplx_t<R>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = 2 * g.m + 1;
-  int hsz = 1;
-#pragma unroll
-  for (int i = 0; i < D; ++i) hsz *= g.H[i];
-  C* halo = reinterpret_cast<C*>(smem_raw);
-  size_t off = align16((size_t)hsz * sizeof(C));
-  C* fval = reinterpret_cast<C*>(smem_raw + off);
-  off += align16(SPREAD_BATCH * sizeof(C));
-  int* hW = reinterpret_cast<int*>(smem_raw + off);  // [batch][2D]: h, W
-  off += align16(SPREAD_BATCH * 2 * D * sizeof(int));
-  R* wb = reinterpret_cast<R*>(smem_raw + off);      // [batch][D*K]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int4 sp = subs[blockIdx.x];
-  int tc[D], org[D];
-  tile_origin<D>(g, sp.x, tc, org);
-  for (int idx = threadIdx.x; idx < hsz; idx += blockDim.x) {
-    C z;
-    z.x = 0;
-    z.y = 0;
-    halo[idx] = z;
-  }
-  const int H1 = D > 1 ? g.H[1] : 1;
-  const int H2 = D > 2 ? g.H[2] : 1;
-  const int end = sp.y + sp.z;
-  for (int base = sp.y; base < end; base += SPREAD_BATCH) {
-    const int nb = min(SPREAD_BATCH, end - base);
-    for (int jb = warp; jb < nb; jb += nwarps) {
-      const int i = base + jb;
-      double x[D];
-#pragma unroll
-      for (int dd = 0; dd < D; ++dd) x[dd] = xs[dd * g.M + i];
-      int h[D], W[D];
-      int64_t lo[D];
-      node_stencil<D>(g, tc, x, h, W, lo);
-      node_weights<R, D>(g, i, x, lo, W, wb + jb * D * K, lane, 32);
-      if (lane == 0) {
-        fval[jb] = fin[perm[i]];
-#pragma unroll
-        for (int dd = 0; dd < D; ++dd) {
-          hW[jb * 2 * D + dd] = h[dd];
-          hW[jb * 2 * D + D + dd] = W[dd];
-        }
-      }
-    }
-    __syncthreads();
-    if constexpr (D == 3) {
-      const int unit = warp, U = nwarps;
-      for (int jb = 0; jb < nb; ++jb) {
-        const int* q = hW + jb * 2 * D;
-        const int h0 = q[0], h1 = q[1], h2 = q[2], W0 = q[3], W1 = q[4], W2 = q[5];
-        const R* w = wb + jb * D * K;
-        const C f = fval[jb];
-        const int P = W1 * W2;
-        for (int a = h0 + ((unit - h0) % U + U) % U; a < h0 + W0; a += U) {
-          R w0 = w[a - h0];
-          R cre = f.x * w0, cim = f.y * w0;
-          for (int p = lane; p < P; p += 32) {
-            int t1 = p / W2, t2 = p - t1 * W2;
-            R ww = w[K + t1] * w[2 * K + t2];
-            C* cell = halo + (a * H1 + h1 + t1) * H2 + h2 + t2;
-            C v = *cell;
-            v.x += cre * ww;
-            v.y += cim * ww;
-            *cell = v;
-          }
-        }
-        __syncwarp();
-      }
-    } else if constexpr (D == 2) {
-      const int unit = threadIdx.x >> 4, U = blockDim.x >> 4, l16 = lane & 15;
-      for (int jb = 0; jb < nb; ++jb) {
-        const int* q = hW + jb * 2 * D;
-        const int h0 = q[0], h1 = q[1], W0 = q[2], W1 = q[3];
-        const R* w = wb + jb * D * K;
-        const C f = fval[jb];
-        for (int a = h0 + ((unit - h0) % U + U) % U; a < h0 + W0; a += U) {
-          R w0 = w[a - h0];
-          R cre = f.x * w0, cim = f.y * w0;
-          for (int t1 = l16; t1 < W1; t1 += 16) {
-            R ww = w[K + t1];
-            C* cell = halo + a * H1 + h1 + t1;
-            C v = *cell;
-            v.x += cre * ww;
-            v.y += cim * ww;
-            *cell = v;
-          }
-        }
-        __syncwarp();
-      }
-    } else {
-      const int unit = threadIdx.x, U = blockDim.x;
-      for (int jb = 0; jb < nb; ++jb) {
-        const int* q = hW + jb * 2 * D;
-        const int h0 = q[0], W0 = q[1];
-        const R* w = wb + jb * D * K;
-        const C f = fval[jb];
-        for (int a = h0 + ((unit - h0) % U + U) % U; a < h0 + W0; a += U) {
-          R w0 = w[a - h0];
-          C v = halo[a];
-          v.x += f.x * w0;
-          v.y += f.y * w0;
-          halo[a] = v;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  for (int idx = threadIdx.x; idx < hsz; idx += blockDim.x) {
-    C v = halo[idx];
-    if (v.x != (R)0 || v.y != (R)0) {
-      int64_t lin = halo_slot<D>(g, org, idx);
-      atomicAdd(&grid[lin].x, v.x);
-      atomicAdd(&grid[lin].y, v.y);
-    }
-  }
-}
-
-size_t interp_smem(const Geom& g, int elem_bytes, int threads) {
-  size_t hsz = 1;
-  for (int i = 0; i < g.d; ++i) hsz *= g.H[i];
-  return ((hsz * elem_bytes + 15) & ~(size_t)15) + (size_t)(threads / 32) * g.d * (2 * g.m + 1) * (elem_bytes / 2);
-}
-
-size_t spread_smem(const Geom& g, int elem_bytes) {
-  size_t hsz = 1;
-  for (int i = 0; i < g.d; ++i) hsz *= g.H[i];
-  size_t off = (hsz * elem_bytes + 15) & ~(size_t)15;
-  off += (SPREAD_BATCH * elem_bytes + 15) & ~(size_t)15;
-  off += (SPREAD_BATCH * 2 * g.d * sizeof(int) + 15) & ~(size_t)15;
-  off += (size_t)SPREAD_BATCH * g.d * (2 * g.m + 1) * (elem_bytes / 2);
-  return off;
-}
-
-template <typename R, int D>
-static void interp_launch(const void* grid, void* f, const double* xs, const int* perm,
-                          const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  const int threads = 256;
-  size_t smem = interp_smem(g, sizeof(cplx_t<R>), threads);
-  auto kern = k_interp_tiled<R, D>;
-  NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (nsubs > 0) {
-    kern<<<nsubs, threads, smem, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)f, xs, perm, subs, g);
-    count_launch();
-  }
-}
-
-template <typename R, int D>
-static void spread_launch(void* grid, const void* f, const double* xs, const int* perm,
-                          const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  const int threads = 256;
-  size_t smem = spread_smem(g, sizeof(cplx_t<R>));
-  auto kern = k_spread_tiled<R, D>;
-  NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (nsubs > 0) {
-    kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)grid, (const cplx_t<R>*)f, xs, perm, subs, g);
-    count_launch();
-  }
-}
-
-void launch_interp(bool single, const void* grid, void* f, const double* xs, const int* perm,
-                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  if (single) {
-    if (g.d == 1) interp_launch<float, 1>(grid, f, xs, perm, subs, nsubs, g, s);
-    else if (g.d == 2) interp_launch<float, 2>(grid, f, xs, perm, subs, nsubs, g, s);
-    else interp_launch<float, 3>(grid, f, xs, perm, subs, nsubs, g, s);
-  } else {
-    if (g.d == 1) interp_launch<double, 1>(grid, f, xs, perm, subs, nsubs, g, s);
-    else if (g.d == 2) interp_launch<double, 2>(grid, f, xs, perm, subs, nsubs, g, s);
-    else interp_launch<double, 3>(grid, f, xs, perm, subs, nsubs, g, s);
-  }
-}
-
-void launch_spread(bool single, void* grid, const void* f, const double* xs, const int* perm,
-                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  if (single) {
-    if (g.d == 1) spread_launch<float, 1>(grid, f, xs, perm, subs, nsubs, g, s);
-    else if (g.d == 2) spread_launch<float, 2>(grid, f, xs, perm, subs, nsubs, g, s);
-    else spread_launch<float, 3>(grid, f, xs, perm, subs, nsubs, g, s);
-  } else {
-    if (g.d == 1) spread_launch<double, 1>(grid, f, xs, perm, subs, nsubs, g, s);
-    else if (g.d == 2) spread_launch<double, 2>(grid, f, xs, perm, subs, nsubs, g, s);
-    else spread_launch<double, 3>(grid, f, xs, perm, subs, nsubs, g, s);
-  }
-}
 
 void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH& qh, cudaStream_t s) {
   DeconvGeom q;

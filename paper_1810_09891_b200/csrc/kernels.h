@@ -17,6 +17,8 @@ struct DeconvGeomH {
 };
 
 unsigned long long launch_count();
+void count_launch();
+int spread_threads(const Geom& g);
 
 void launch_check_range(const double* x, int64_t count, unsigned long long* first_bad,
                         cudaStream_t s);
@@ -31,8 +33,8 @@ void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH&
 void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& q, cudaStream_t s);
 void launch_interp(bool single, const void* grid, void* f, const double* xs, const int* perm,
                    const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
-void launch_spread(bool single, void* grid, const void* f, const double* xs, const int* perm,
-                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+void launch_spread(bool single, void* grid, const void* f, void* fs, const double* xs,
+                   const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
 
 double measure_fma_tflops(bool fp64);
 

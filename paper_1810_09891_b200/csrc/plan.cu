@@ -116,6 +116,7 @@ Plan::~Plan() {
   if (!grid_external) cudaFree(grid);
   cudaFree(fhat_dev);
   cudaFree(f_dev);
+  cudaFree(f_sorted);
   if (fhat_pinned) cudaFreeHost(fhat_host); else free(fhat_host);
   if (f_pinned) cudaFreeHost(f_host); else free(f_host);
   for (auto& r : recs) { event_pool.push_back(r.a); event_pool.push_back(r.b); }
@@ -128,19 +129,39 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-// Tile edge per dim: the largest power of two whose (T+2m+1)^d halo fits the
-// shared-memory budget (two CTAs per SM at the default budget).
+// Tile edge per dim (powers of two).  d = 3: the smallest tile expected to
+// hold >= 64 nodes whose halo fits 100 KB (two CTAs per SM), else the largest
+// halo up to 190 KB (one CTA per SM, 16 warps) -- low node densities need big
+// tiles to amortise the halo.  d = 2 / d = 1: the largest halo within
+// 100 KB / 64 KB.  NFFTK_TILE overrides.
 static void choose_tiles(Plan* p) {
   Geom& g = p->geom;
-  size_t budget = (size_t)env_int("NFFTK_HALO_KB", 100) * 1024;
-  int force = env_int("NFFTK_TILE", 0);
-  int start = p->d == 3 ? 16 : (p->d == 2 ? 128 : 4096);
-  int T = start;
-  for (; T > 1; T /= 2) {
+  const size_t KB = 1024;
+  const size_t eb = p->elem_bytes();
+  const double rho = (double)p->M / (double)p->grid_size;
+  auto halo_bytes = [&](int T) {
     size_t h = 1;
     for (int i = 0; i < p->d; ++i) h *= (size_t)(std::min(T, p->n[i]) + 2 * p->m + 1);
-    if (h * p->elem_bytes() <= budget) break;
+    return h * eb;
+  };
+  int T = 0;
+  if (p->d == 3) {
+    for (int c : {4, 8, 16})
+      if (rho * c * c * c >= 64.0 && halo_bytes(c) <= 100 * KB) { T = c; break; }
+    if (!T)
+      for (int c : {16, 8, 4, 2})
+        if (halo_bytes(c) <= 190 * KB) { T = c; break; }
+    if (!T) T = 2;
+  } else if (p->d == 2) {
+    for (int c : {128, 64, 32, 16, 8, 4, 2})
+      if (halo_bytes(c) <= 100 * KB) { T = c; break; }
+    if (!T) T = 2;
+  } else {
+    for (int c = 4096; c >= 2; c /= 2)
+      if (halo_bytes(c) <= 64 * KB) { T = c; break; }
+    if (!T) T = 2;
   }
+  int force = env_int("NFFTK_TILE", 0);
   if (force > 0) T = force;
   p->ntiles = 1;
   for (int i = 0; i < p->d; ++i) {
@@ -149,6 +170,8 @@ static void choose_tiles(Plan* p) {
     g.ntile[i] = (p->n[i] + g.T[i] - 1) / g.T[i];
     p->ntiles *= g.ntile[i];
   }
+  g.nt_interp = interp_smem(g, (int)eb, 256) > 110 * KB ? 512 : 256;
+  g.nt_interp = env_int("NFFTK_INTERP_THREADS", g.nt_interp);
   p->maxsub = env_int("NFFTK_MAXSUB", 1024);
 }
 
@@ -510,7 +533,8 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   { PhaseScope ps(p, PH_ZERO, s);
     NFFTK_CUDA(cudaMemsetAsync(p->grid, 0, p->elem_bytes() * p->grid_size, s)); }
   { PhaseScope ps(p, PH_SPREAD, s);
-    launch_spread(p->single, p->grid, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+    if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * p->M));
+    launch_spread(p->single, p->grid, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }

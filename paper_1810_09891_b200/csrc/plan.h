@@ -59,6 +59,7 @@ struct Plan {
   bool grid_external = false;
   void* fhat_dev = nullptr;
   void* f_dev = nullptr;
+  void* f_sorted = nullptr;         // spread input in tile-sorted order
   cufftHandle fft = 0;
   bool fft_ready = false;
 
