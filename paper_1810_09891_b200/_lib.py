@@ -63,7 +63,8 @@ SIGNATURES = {
     "nfftk_live_buffers": (_i64, []),
 }
 
-PHASES = ("deconv", "fft_fwd", "interp", "zero", "spread", "fft_inv", "pack", "h2d", "d2h")
+PHASES = ("deconv", "fft_fwd", "interp", "zero", "spread", "fft_inv", "pack", "h2d", "d2h",
+          "pad", "fold")
 
 _lib = None
 

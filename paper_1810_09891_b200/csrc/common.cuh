@@ -119,6 +119,9 @@ struct Geom {
   const double* psi;      // M * d * (2m+1) in sorted order (MODE_TENSOR)
   int64_t M;
   int nt_interp;          // threads per interp CTA
+  int np[MAX_D];          // ghost-padded grid (periodic images, halo = one box)
+  int HS;                 // halo row stride (elements) of the last dim
+  int nb_spread;          // spread node batch size
 };
 
 // -------------------------------------------------------- device window

@@ -5,18 +5,24 @@
 //
 // Both work on tile subproblems produced by the device sort (kernels.cu):
 // one CTA per (tile, <= maxsub nodes).  The tile's (T + 2m + 1)^d halo lives
-// in shared memory.  With T even the halo row length is odd, which keeps the
-// lane-strided 128-bit row accesses bank-conflict free.
+// in shared memory.  The grid they read / write is the ghost-padded copy
+// (plan.cu: pad / fold kernels keep the periodic images), so every halo is
+// ONE contiguous box:
+//   * interp loads it with a single TMA tensor copy (cp.async.bulk.tensor,
+//     completion on an mbarrier);
+//   * spread flushes it with TMA bulk fp64 (fp32) reductions into L2
+//     (cp.reduce.async.bulk .add), one per halo row -- no per-cell atomics.
+// Node batches (coordinates, samples, PRE_PSI factors) arrive by cp.async into
+// a double buffer while the previous batch is processed.
 //
-// Data movement: the interp halo arrives by TMA bulk copies (one
-// cp.async.bulk per contiguous halo row, completion on an mbarrier); node
-// batches (coordinates, samples, PRE_PSI factors) arrive by cp.async into a
-// double buffer while the previous batch is being processed.
-//
+// Halo rows along the last dimension have stride HS (= H for complex128,
+// which is odd and keeps lane-strided 128-bit accesses bank-conflict free).
 // Kernels are templated on the cutoff MM (1..8; 0 = runtime m) so the 2m-wide
-// stencil loops unroll.  Nodes whose stencil is 2m+1 wide in some dimension
-// (n x an exact integer, or fp rounding at the edges -- see common.cuh
+// stencil loops unroll; nodes whose stencil is 2m+1 wide in some dimension
+// (n x an exact integer, or fp rounding at the edges -- common.cuh
 // ``stencil``) take a generic path with runtime widths.
+#include <cuda.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -24,33 +30,15 @@
 
 namespace nfftk {
 
-__device__ __forceinline__ int wrapi(int v, int n) {
-  v %= n;
-  return v < 0 ? v + n : v;
-}
-
 __device__ __forceinline__ size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 template <int D>
-__device__ __forceinline__ void tile_of(const Geom& g, int tile, int* tc, int* org) {
+__device__ __forceinline__ void tile_of(const Geom& g, int tile, int* tc) {
   int t = tile;
 #pragma unroll
   for (int i = D - 1; i >= 0; --i) {
     tc[i] = t % g.ntile[i];
     t /= g.ntile[i];
-  }
-#pragma unroll
-  for (int i = 0; i < D; ++i) org[i] = tc[i] * g.T[i] - g.m;
-}
-
-// wrapped grid slot of every halo coordinate, per dimension
-template <int D>
-__device__ __forceinline__ void build_slots(const Geom& g, const int* org, int* slots) {
-  int off = 0;
-#pragma unroll
-  for (int dim = 0; dim < D; ++dim) {
-    for (int a = threadIdx.x; a < g.H[dim]; a += blockDim.x) slots[off + a] = wrapi(org[dim] + a, g.n[dim]);
-    off += g.H[dim];
   }
 }
 
@@ -95,7 +83,26 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
-// TMA bulk copy global -> shared (size multiple of 16, both 16-B aligned)
+
+// TMA: whole halo box of the padded grid -> shared memory
+template <int D>
+__device__ __forceinline__ void tma_load_box(void* sdst, const CUtensorMap* tm, const int* c,
+                                             unsigned long long* bar) {
+  if constexpr (D == 3) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(sdst)),
+        "l"(tm), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(smem_u32(bar))
+        : "memory");
+  } else if constexpr (D == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(sdst)),
+        "l"(tm), "r"(c[0]), "r"(c[1]), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes,
                                          unsigned long long* bar) {
   asm volatile(
@@ -105,66 +112,43 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
       : "memory");
 }
 
-// Halo staging.  complex128: one bulk copy per contiguous piece of a halo
-// row (rows along the last dim; a row splits where it wraps).  complex64
-// rows are not 16-byte multiples: per-cell cp.async.
-template <typename C, int D>
-__device__ __forceinline__ void issue_halo(const Geom& g, const C* __restrict__ grid, const int* slots,
-                                           C* halo, unsigned long long* bar) {
-  const int H0 = g.H[0];
-  const int HL = g.H[D - 1];
-  const int nl = g.n[D - 1];
-  const int rows = D == 1 ? 1 : (D == 2 ? H0 : H0 * g.H[1]);
-  const int* sl = slots + (D == 1 ? 0 : (D == 2 ? H0 : H0 + g.H[1]));
-  if constexpr (sizeof(C) == 16) {
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-      int64_t rbase = 0;
-      if constexpr (D == 2) {
-        rbase = (int64_t)slots[r] * g.n[1];
-      } else if constexpr (D == 3) {
-        int a = r / g.H[1], b = r - a * g.H[1];
-        rbase = ((int64_t)slots[a] * g.n[1] + slots[H0 + b]) * g.n[2];
-      }
-      C* dst = halo + (size_t)r * HL;
-      int c = 0;
-      while (c < HL) {
-        int s = sl[c];
-        int len = min(HL - c, nl - s);
-        bulk_g2s(dst + c, grid + rbase + s, (unsigned)(len * sizeof(C)), bar);
-        c += len;
-      }
-    }
-  } else {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int r = warp; r < rows; r += nwarps) {
-      int64_t rbase = 0;
-      if constexpr (D == 2) {
-        rbase = (int64_t)slots[r] * g.n[1];
-      } else if constexpr (D == 3) {
-        int a = r / g.H[1], b = r - a * g.H[1];
-        rbase = ((int64_t)slots[a] * g.n[1] + slots[H0 + b]) * g.n[2];
-      }
-      for (int c = lane; c < HL; c += 32) cp_async_cell(halo + (size_t)r * HL + c, grid + rbase + sl[c]);
-    }
-  }
+// TMA bulk reduction shared -> global (L2 performs the adds)
+template <typename R>
+__device__ __forceinline__ void bulk_red_add(void* gdst, const void* ssrc, unsigned bytes) {
+  if constexpr (sizeof(R) == 8)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::);
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// Node batch buffers: coordinates, (interp) output index / (spread) sorted
-// samples, window factors (copied from the PRE_PSI table, or computed) and
-// per-node stencil data hw = {h_0..h_{D-1}, W_0..W_{D-1}, h_0 mod UA}.
+// ----------------------------------------------------------- node batches
+// coordinates [D][NB], window factors [NB][D*K] (PRE_PSI rows copied, or
+// computed), stencil data hw[NB][2D+1] = {h_0..h_{D-1}, W_0..W_{D-1}, fast},
+// interp output index pb[NB], spread sorted samples fv[NB].
 template <typename C, int D>
 struct Batch {
-  double* x;   // [D][NB]
-  double* w;   // [NB][D*K]
-  int* hw;     // [NB][2D+1]
-  int* pb;     // [NB] interp: output index
-  C* fv;       // [NB] spread: sorted samples
+  double* x;
+  double* w;
+  int* hw;
+  int* pb;
+  C* fv;
 };
 
 __host__ __device__ inline size_t batch_bytes_of(int d, int nb, int K, int elem) {
   auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
   return al(sizeof(double) * d * nb) + al(sizeof(double) * nb * d * K) +
-         al(sizeof(int) * nb * (2 * d + 1)) + al(sizeof(int) * nb) + al((size_t)elem * nb);
+         al(sizeof(int) * nb * (2 * d + 2)) + al(sizeof(int) * nb) + al((size_t)elem * nb);
 }
 
 template <typename C, int D>
@@ -175,14 +159,13 @@ __device__ __forceinline__ Batch<C, D> batch_at(unsigned char* p, int nb, int K)
   b.w = reinterpret_cast<double*>(p);
   p += a16(sizeof(double) * nb * D * K);
   b.hw = reinterpret_cast<int*>(p);
-  p += a16(sizeof(int) * nb * (2 * D + 1));
+  p += a16(sizeof(int) * nb * (2 * D + 2));
   b.pb = reinterpret_cast<int*>(p);
   p += a16(sizeof(int) * nb);
   b.fv = reinterpret_cast<C*>(p);
   return b;
 }
 
-// Issue the asynchronous copies of batch [base, base+nb).
 template <typename C, int D>
 __device__ __forceinline__ void issue_batch(const Geom& g, const double* __restrict__ xs,
                                             const int* __restrict__ perm, const C* __restrict__ fs,
@@ -203,20 +186,25 @@ __device__ __forceinline__ void issue_batch(const Geom& g, const double* __restr
 }
 
 // Stencils in halo coordinates, h = (cell slot - tile start) + m - (cell - lo)
-// in [0, T + m + 1], and (DIRECT / LUT) the window factors, from the staged
-// coordinates (kernels.py:42-53 for a whole batch).  hw[2D] = h_0 mod ua.
+// in [0, T + m + 1]; the fast flag (width 2m in every dim); (DIRECT / LUT)
+// window factors -- kernels.py:42-53 for a whole batch.
 template <typename C, int D>
 __device__ __forceinline__ void finish_batch(const Geom& g, const int* tc, int nb, int NB, int ua,
                                              const Batch<C, D>& b) {
   const int K = 2 * g.m + 1, per = D * K;
-  for (int q = threadIdx.x; q < nb * D; q += blockDim.x) {
-    int j = q / D, dim = q - j * D;
-    Stencil st = stencil(b.x[dim * NB + j], g.nd[dim], g.md);
-    int slot = (int)floor_mod(st.cell, g.n[dim]);
-    int h = slot - tc[dim] * g.T[dim] + g.m - (int)(st.cell - st.lo);
-    b.hw[j * (2 * D + 1) + dim] = h;
-    b.hw[j * (2 * D + 1) + D + dim] = st.width;
-    if (dim == 0) b.hw[j * (2 * D + 1) + 2 * D] = h % ua;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+    bool fast = true;
+    int* q = b.hw + j * (2 * D + 2);
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) {
+      Stencil st = stencil(b.x[dim * NB + j], g.nd[dim], g.md);
+      int slot = (int)floor_mod(st.cell, g.n[dim]);
+      q[dim] = slot - tc[dim] * g.T[dim] + g.m - (int)(st.cell - st.lo);
+      q[D + dim] = st.width;
+      fast = fast && st.width == 2 * g.m;
+    }
+    q[2 * D] = fast;
+    q[2 * D + 1] = q[0] % ua;
   }
   if (g.mode != MODE_TENSOR) {
     for (int q = threadIdx.x; q < nb * per; q += blockDim.x) {
@@ -226,14 +214,6 @@ __device__ __forceinline__ void finish_batch(const Geom& g, const int* tc, int n
       b.w[q] = t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0;
     }
   }
-}
-
-template <int D>
-__device__ __forceinline__ bool is_fast(const int* q, int m) {
-  bool f = true;
-#pragma unroll
-  for (int i = 0; i < D; ++i) f = f && q[D + i] == 2 * m;
-  return f;
 }
 
 // Lanes per node in the interp: enough work per lane to amortise the
@@ -247,7 +227,7 @@ struct InterpTeam {
 };
 
 // ======================================================== B: interpolation
-// One CTA per subproblem.  The halo arrives by TMA bulk copies while the first
+// One CTA per subproblem.  One TMA copy brings the halo box while the first
 // node batch arrives by cp.async; the next batch is fetched while the current
 // one is processed.  A team of TEAM lanes reduces one node: lanes split the
 // leading stencil dims and run along the contiguous last dim with the factors
@@ -256,65 +236,70 @@ constexpr int INTERP_NB = 32;
 
 template <typename R, int D, int MM>
 __global__ void __launch_bounds__(512)
-k_interp(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
-         const double* __restrict__ xs, const int* __restrict__ perm,
+k_interp(const __grid_constant__ CUtensorMap tmap, const cplx_t<R>* __restrict__ gp,
+         cplx_t<R>* __restrict__ fout, const double* __restrict__ xs, const int* __restrict__ perm,
          const int4* __restrict__ subs, Geom g) {
   using C = cplx_t<R>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int m = MM ? MM : g.m;
   const int K = 2 * m + 1;
-  const int H0 = g.H[0], H1 = D > 1 ? g.H[1] : 1, H2 = D > 2 ? g.H[2] : 1;
-  const int hsz = H0 * H1 * H2;
-  const int nslots = H0 + (D > 1 ? H1 : 0) + (D > 2 ? H2 : 0);
-  size_t off = 0;
+  const int HS = g.HS;
+  const int H0 = g.H[0], H1 = D > 2 ? g.H[1] : 1;
+  const int rows = D == 1 ? 1 : (D == 2 ? H0 : H0 * H1);
+  const size_t hbytes = a16((size_t)rows * HS * sizeof(C));
   C* halo = reinterpret_cast<C*>(smem);
-  off += a16((size_t)hsz * sizeof(C));
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + off);
-  off += 16;
-  int* slots = reinterpret_cast<int*>(smem + off);
-  off += a16(nslots * sizeof(int));
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + hbytes);
+  unsigned char* bufbase = smem + hbytes + 16;
   const size_t bb = batch_bytes_of(D, INTERP_NB, K, sizeof(C));
-  Batch<C, D> buf[2] = {batch_at<C, D>(smem + off, INTERP_NB, K),
-                        batch_at<C, D>(smem + off + bb, INTERP_NB, K)};
   constexpr int TEAM = InterpTeam<D, MM>::value;
   constexpr int NPW = 32 / TEAM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int tl = lane % TEAM, sub = lane / TEAM;
   const int4 sp = subs[blockIdx.x];
-  int tc[D], org[D];
-  tile_of<D>(g, sp.x, tc, org);
-  build_slots<D>(g, org, slots);
+  int tc[D];
+  tile_of<D>(g, sp.x, tc);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    if (sizeof(C) == 16) mbar_expect_tx(bar, (unsigned)(hsz * sizeof(C)));
+    mbar_expect_tx(bar, (unsigned)((size_t)rows * HS * sizeof(C)));
+    if constexpr (D == 1) {
+      bulk_g2s(halo, gp + tc[0] * g.T[0], (unsigned)(HS * sizeof(C)), bar);
+    } else {
+      // padded-grid origin of the halo is tile * T; innermost coordinate in
+      // 8-byte units (complex128 = two float64)
+      int c[3];
+      const int scale = sizeof(C) / 8;
+#pragma unroll
+      for (int i = 0; i < D; ++i) c[D - 1 - i] = tc[i] * g.T[i];
+      c[0] *= scale;
+      tma_load_box<D>(halo, &tmap, c, bar);
+    }
   }
-  __syncthreads();
-  issue_halo<C, D>(g, grid, slots, halo, bar);
   const int end = sp.y + sp.z;
-  issue_batch<C, D>(g, xs, perm, nullptr, sp.y, min(INTERP_NB, sp.z), INTERP_NB, buf[0]);
+  issue_batch<C, D>(g, xs, perm, nullptr, sp.y, min(INTERP_NB, sp.z), INTERP_NB,
+                    batch_at<C, D>(bufbase, INTERP_NB, K));
   cp_async_commit();
   int k = 0;
   for (int base = sp.y; base < end; base += INTERP_NB, ++k) {
     const int nb = min(INTERP_NB, end - base);
-    const Batch<C, D>& cur = buf[k & 1];
+    const Batch<C, D> cur = batch_at<C, D>(bufbase + (k & 1) * bb, INTERP_NB, K);
     cp_async_wait_all();
     __syncthreads();
     finish_batch<C, D>(g, tc, nb, INTERP_NB, 1, cur);
     __syncthreads();
     if (base + INTERP_NB < end) {
       issue_batch<C, D>(g, xs, perm, nullptr, base + INTERP_NB, min(INTERP_NB, end - base - INTERP_NB),
-                        INTERP_NB, buf[(k + 1) & 1]);
+                        INTERP_NB, batch_at<C, D>(bufbase + ((k + 1) & 1) * bb, INTERP_NB, K));
       cp_async_commit();
     }
-    if (k == 0 && sizeof(C) == 16) mbar_wait(bar, 0);
+    if (k == 0) mbar_wait(bar, 0);
     for (int j0 = warp * NPW; j0 < nb; j0 += nwarps * NPW) {
       const int jb = j0 + sub;
       const bool active = jb < nb;
-      const int* q = cur.hw + (active ? jb : j0) * (2 * D + 1);
+      const int* q = cur.hw + (active ? jb : j0) * (2 * D + 2);
       const double* w = cur.w + (active ? jb : j0) * D * K;
       R are = 0, aim = 0;
       if (active) {
-        if (MM > 0 && is_fast<D>(q, m)) {
+        if (MM > 0 && q[2 * D]) {
           constexpr int WF = 2 * (MM > 0 ? MM : 1);
           if constexpr (D == 1) {
             for (int t0 = tl; t0 < WF; t0 += TEAM) {
@@ -327,7 +312,7 @@ k_interp(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
             constexpr int SEG = WF / 2;
             for (int p = tl; p < 2 * WF; p += TEAM) {
               int t0 = p >> 1, seg = p & 1;
-              const C* row = halo + (q[0] + t0) * H1 + q[1] + seg * SEG;
+              const C* row = halo + (q[0] + t0) * HS + q[1] + seg * SEG;
               const double* w1 = w + K + seg * SEG;
               R sre = 0, sim = 0;
 #pragma unroll
@@ -345,11 +330,11 @@ k_interp(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
             R w2r[WF];
 #pragma unroll
             for (int t = 0; t < WF; ++t) w2r[t] = (R)w[2 * K + t];
-            const C* corner = halo + (q[0] * H1 + q[1]) * H2 + q[2];
+            const C* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
 #pragma unroll 2
             for (int p = tl; p < WF * WF; p += TEAM) {
               int t0 = p / WF, t1 = p - t0 * WF;
-              const C* row = corner + (t0 * H1 + t1) * H2;
+              const C* row = corner + (t0 * H1 + t1) * HS;
               R sre = 0, sim = 0;
 #pragma unroll
               for (int t = 0; t < WF; ++t) {
@@ -378,8 +363,8 @@ k_interp(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
             const double* wl = w + (D - 1) * K;
             for (int p = tl; p < P; p += TEAM) {
               int t0 = p / W1, t1 = p - t0 * W1;
-              const C* row = D == 2 ? halo + (q[0] + t0) * H1 + q[1]
-                                    : halo + ((q[0] + t0) * H1 + q[1] + t1) * H2 + q[D - 1];
+              const C* row = D == 2 ? halo + (q[0] + t0) * HS + q[1]
+                                    : halo + ((q[0] + t0) * H1 + q[1] + t1) * HS + q[D - 1];
               R sre = 0, sim = 0;
               for (int t = 0; t < WL; ++t) {
                 C v = row[t];
@@ -406,7 +391,6 @@ k_interp(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fout,
       }
     }
   }
-  if (sp.z <= 0 && sizeof(C) == 16) mbar_wait(bar, 0);
 }
 
 // Sorted copy of the samples for the spread: fs[i] = f[perm[i]].
@@ -424,222 +408,224 @@ __global__ void k_permute_samples(const C* __restrict__ f, const int* __restrict
 // so a generic node gives every warp exactly one a-row; d=2: half-warps own
 // a mod U; d=1: threads own cells mod U), so two warps never touch the same
 // cell -- the GPU form of the reference's slab ownership (kernels.py:13-17).
-// Node batches (coordinates, sorted samples, factors) arrive by cp.async,
-// double-buffered.  The finished halo is added to the HBM grid with fp64
-// (fp32) RED atomics, skipping untouched cells.
-constexpr int SPREAD_NB = 32;
-
+// Per batch the CTA stages, for every node, the complex row coefficients
+// f_j * w0[t] and (d=3, generic nodes) the w1 (x) w2 factor plane, so each
+// warp's per-node work is a handful of loads plus one 5-instruction
+// read-modify-write per cell.  The finished halo is added to the padded HBM
+// grid with TMA bulk reductions, one per halo row.
 template <typename R, int D, int MM>
 __global__ void __launch_bounds__(512)
-k_spread(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted,
+k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
          const double* __restrict__ xs, const int4* __restrict__ subs, Geom g) {
   using C = cplx_t<R>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int m = MM ? MM : g.m;
   const int K = 2 * m + 1;
-  const int H0 = g.H[0], H1 = D > 1 ? g.H[1] : 1, H2 = D > 2 ? g.H[2] : 1;
-  const int hsz = H0 * H1 * H2;
-  const int nslots = H0 + (D > 1 ? H1 : 0) + (D > 2 ? H2 : 0);
+  constexpr int WF = 2 * (MM > 0 ? MM : 1);
+  const int NB = g.nb_spread;
+  const int HS = g.HS;
+  const int H0 = g.H[0], H1 = D > 2 ? g.H[1] : 1;
+  const int rows = D == 1 ? 1 : (D == 2 ? H0 : H0 * H1);
+  const int hsz = rows * HS;
   size_t off = 0;
   C* halo = reinterpret_cast<C*>(smem);
   off += a16((size_t)hsz * sizeof(C));
-  int* slots = reinterpret_cast<int*>(smem + off);
-  off += a16(nslots * sizeof(int));
-  const size_t bb = batch_bytes_of(D, SPREAD_NB, K, sizeof(C));
-  Batch<C, D> buf[2] = {batch_at<C, D>(smem + off, SPREAD_NB, K),
-                        batch_at<C, D>(smem + off + bb, SPREAD_NB, K)};
+  C* coef = reinterpret_cast<C*>(smem + off);          // [NB][K]  f * w0[t]
+  off += a16((size_t)NB * K * sizeof(C));
+  double* plane = reinterpret_cast<double*>(smem + off);  // [NB][WF*WF] (d=3)
+  off += D == 3 ? a16((size_t)NB * WF * WF * sizeof(double)) : 0;
+  unsigned char* bufbase = smem + off;
+  const size_t bb = batch_bytes_of(D, NB, K, sizeof(C));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int4 sp = subs[blockIdx.x];
-  int tc[D], org[D];
-  tile_of<D>(g, sp.x, tc, org);
+  int tc[D];
+  tile_of<D>(g, sp.x, tc);
   const int end = sp.y + sp.z;
-  issue_batch<C, D>(g, xs, nullptr, fsorted, sp.y, min(SPREAD_NB, sp.z), SPREAD_NB, buf[0]);
+  issue_batch<C, D>(g, xs, nullptr, fsorted, sp.y, min(NB, sp.z), NB, batch_at<C, D>(bufbase, NB, K));
   cp_async_commit();
-  build_slots<D>(g, org, slots);
   for (int idx = threadIdx.x; idx < hsz; idx += blockDim.x) {
     C z;
     z.x = 0;
     z.y = 0;
     halo[idx] = z;
   }
-  const int UA = D == 3 ? nwarps : (D == 2 ? (int)(blockDim.x >> 4) : (int)blockDim.x);
+  const int UA = D == 3 ? nwarps : 1;
+  // per-lane cell offsets inside a node's (b, c) plane, fast path (d=3)
+  constexpr int NK = (WF * WF + 31) / 32;
+  int offk[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) {
+    int p = lane + 32 * kk;
+    int t1 = p / WF, t2 = p - t1 * WF;
+    offk[kk] = t1 * HS + t2;
+  }
   int k = 0;
-  for (int base = sp.y; base < end; base += SPREAD_NB, ++k) {
-    const int nb = min(SPREAD_NB, end - base);
-    const Batch<C, D>& cur = buf[k & 1];
+  for (int base = sp.y; base < end; base += NB, ++k) {
+    const int nb = min(NB, end - base);
+    const Batch<C, D> cur = batch_at<C, D>(bufbase + (k & 1) * bb, NB, K);
     cp_async_wait_all();
     __syncthreads();  // batch k landed; previous batch applied; zeroing done
-    finish_batch<C, D>(g, tc, nb, SPREAD_NB, UA, cur);
+    finish_batch<C, D>(g, tc, nb, NB, UA, cur);
     __syncthreads();
-    if (base + SPREAD_NB < end) {
-      issue_batch<C, D>(g, xs, nullptr, fsorted, base + SPREAD_NB,
-                        min(SPREAD_NB, end - base - SPREAD_NB), SPREAD_NB, buf[(k + 1) & 1]);
+    // derived per-node data: row coefficients, factor plane
+    for (int q = threadIdx.x; q < nb * K; q += blockDim.x) {
+      int j = q / K, t = q - j * K;
+      R w0 = (R)cur.w[j * D * K + t];
+      C f = cur.fv[j];
+      C c;
+      c.x = f.x * w0;
+      c.y = f.y * w0;
+      coef[q] = c;
+    }
+    if constexpr (D == 3) {
+      if (MM > 0) {
+        for (int q = threadIdx.x; q < nb * WF * WF; q += blockDim.x) {
+          int j = q / (WF * WF), p = q - j * (WF * WF), t1 = p / WF, t2 = p - t1 * WF;
+          plane[q] = cur.w[j * D * K + K + t1] * cur.w[j * D * K + 2 * K + t2];
+        }
+      }
+    }
+    __syncthreads();
+    if (base + NB < end) {
+      issue_batch<C, D>(g, xs, nullptr, fsorted, base + NB, min(NB, end - base - NB), NB,
+                        batch_at<C, D>(bufbase + ((k + 1) & 1) * bb, NB, K));
       cp_async_commit();
     }
     if constexpr (D == 3) {
       for (int jb = 0; jb < nb; ++jb) {
-        const int* q = cur.hw + jb * (2 * D + 1);
-        const int h0 = q[0], h1 = q[1], h2 = q[2], W0 = q[3], W1 = q[4], W2 = q[5];
-        const double* w = cur.w + jb * D * K;
-        const C f = cur.fv[jb];
-        int d0 = warp - q[6];
+        const int* q = cur.hw + jb * (2 * D + 2);
+        const int h0 = q[0];
+        int d0 = warp - q[7];
         if (d0 < 0) d0 += UA;
-        for (int a = h0 + d0; a < h0 + W0; a += UA) {
-          R w0 = (R)w[a - h0];
-          R cre = f.x * w0, cim = f.y * w0;
-          C* plane = halo + (a * H1 + h1) * H2 + h2;
-          if (MM > 0 && W1 == 2 * m && W2 == 2 * m) {
-            constexpr int WF = 2 * (MM > 0 ? MM : 1);
+        if (MM > 0 && q[6] && UA == WF) {
+          // generic node: exactly one owned row a = h0 + d0
+          const C cf = coef[jb * K + d0];
+          C* cellp = halo + ((h0 + d0) * H1 + q[1]) * HS + q[2];
+          const double* pl = plane + jb * WF * WF;
 #pragma unroll
-            for (int p = lane; p < WF * WF; p += 32) {
-              int t1 = p / WF, t2 = p - t1 * WF;
-              R ww = (R)(w[K + t1] * w[2 * K + t2]);
-              C* cell = plane + t1 * H2 + t2;
+          for (int kk = 0; kk < NK; ++kk) {
+            if (kk < NK - 1 || lane + 32 * kk < WF * WF) {
+              R ww = (R)pl[lane + 32 * kk];
+              C* cell = cellp + offk[kk];
               C v = *cell;
-              v.x = fma(cre, ww, v.x);
-              v.y = fma(cim, ww, v.y);
-              *cell = v;
-            }
-          } else {
-            for (int p = lane; p < W1 * W2; p += 32) {
-              int t1 = p / W2, t2 = p - t1 * W2;
-              R ww = (R)(w[K + t1] * w[2 * K + t2]);
-              C* cell = plane + t1 * H2 + t2;
-              C v = *cell;
-              v.x = fma(cre, ww, v.x);
-              v.y = fma(cim, ww, v.y);
+              v.x = fma(cf.x, ww, v.x);
+              v.y = fma(cf.y, ww, v.y);
               *cell = v;
             }
           }
-        }
-        __syncwarp();
-      }
-    } else if constexpr (D == 2) {
-      const int unit = threadIdx.x >> 4, U = UA, l16 = lane & 15;
-      for (int jb = 0; jb < nb; ++jb) {
-        const int* q = cur.hw + jb * (2 * D + 1);
-        const int h0 = q[0], h1 = q[1], W0 = q[2], W1 = q[3];
-        const double* w = cur.w + jb * D * K;
-        const C f = cur.fv[jb];
-        int d0 = unit - q[4];
-        if (d0 < 0) d0 += U;
-        for (int a = h0 + d0; a < h0 + W0; a += U) {
-          R w0 = (R)w[a - h0];
-          R cre = f.x * w0, cim = f.y * w0;
-          C* row = halo + a * H1 + h1;
-          for (int t1 = l16; t1 < W1; t1 += 16) {
-            R ww = (R)w[K + t1];
-            C v = row[t1];
-            v.x = fma(cre, ww, v.x);
-            v.y = fma(cim, ww, v.y);
-            row[t1] = v;
+        } else {
+          const int h1 = q[1], h2 = q[2], W0 = q[3], W1 = q[4], W2 = q[5];
+          const double* w = cur.w + jb * D * K;
+          for (int a = h0 + d0; a < h0 + W0; a += UA) {
+            const C cf = coef[jb * K + (a - h0)];
+            C* pl = halo + (a * H1 + h1) * HS + h2;
+            for (int p = lane; p < W1 * W2; p += 32) {
+              int t1 = p / W2, t2 = p - t1 * W2;
+              R ww = (R)(w[K + t1] * w[2 * K + t2]);
+              C* cell = pl + t1 * HS + t2;
+              C v = *cell;
+              v.x = fma(cf.x, ww, v.x);
+              v.y = fma(cf.y, ww, v.y);
+              *cell = v;
+            }
           }
         }
         __syncwarp();
       }
     } else {
-      const int unit = threadIdx.x, U = UA;
+      // d = 1, 2: the CTA is one warp with a private halo; one node at a time,
+      // lanes over the node's stencil cells (distinct cells, no conflicts)
       for (int jb = 0; jb < nb; ++jb) {
-        const int* q = cur.hw + jb * (2 * D + 1);
-        const int h0 = q[0], W0 = q[1];
+        const int* q = cur.hw + jb * (2 * D + 2);
         const double* w = cur.w + jb * D * K;
-        const C f = cur.fv[jb];
-        int d0 = unit - q[2];
-        if (d0 < 0) d0 += U;
-        for (int a = h0 + d0; a < h0 + W0; a += U) {
-          R w0 = (R)w[a - h0];
-          C v = halo[a];
-          v.x = fma(f.x, w0, v.x);
-          v.y = fma(f.y, w0, v.y);
-          halo[a] = v;
+        if constexpr (D == 2) {
+          const int W0 = q[2], W1 = q[3];
+          C* corner = halo + q[0] * HS + q[1];
+          for (int p = lane; p < W0 * W1; p += 32) {
+            int t0 = p / W1, t1 = p - t0 * W1;
+            const C cf = coef[jb * K + t0];
+            R ww = (R)w[K + t1];
+            C* cell = corner + t0 * HS + t1;
+            C v = *cell;
+            v.x = fma(cf.x, ww, v.x);
+            v.y = fma(cf.y, ww, v.y);
+            *cell = v;
+          }
+        } else {
+          const int W0 = q[1];
+          for (int t0 = lane; t0 < W0; t0 += 32) {
+            const C cf = coef[jb * K + t0];
+            C* cell = halo + q[0] + t0;
+            C v = *cell;
+            v.x += cf.x;
+            v.y += cf.y;
+            *cell = v;
+          }
         }
+        __syncwarp();
       }
     }
   }
+  // ---- flush: one TMA bulk reduction per halo row into the padded grid
+  fence_proxy_async_smem();
   __syncthreads();
-  // ---- flush: rows of the halo, RED atomics into the wrapped grid slots
-  if constexpr (D == 1) {
-    for (int c = threadIdx.x; c < H0; c += blockDim.x) {
-      C v = halo[c];
-      if (v.x != (R)0 || v.y != (R)0) {
-        atomicAdd(&grid[slots[c]].x, v.x);
-        atomicAdd(&grid[slots[c]].y, v.y);
-      }
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    int64_t row0;
+    if constexpr (D == 1) {
+      row0 = (int64_t)tc[0] * g.T[0];
+    } else if constexpr (D == 2) {
+      row0 = (int64_t)(tc[0] * g.T[0] + r) * g.np[1] + tc[1] * g.T[1];
+    } else {
+      int a = r / H1, b = r - a * H1;
+      row0 = ((int64_t)(tc[0] * g.T[0] + a) * g.np[1] + tc[1] * g.T[1] + b) * g.np[2] + tc[2] * g.T[2];
     }
-  } else {
-    const int rows = D == 2 ? H0 : H0 * H1;
-    const int HL = D == 2 ? H1 : H2;
-    const int* sl = slots + H0 + (D == 3 ? H1 : 0);
-    for (int r = warp; r < rows; r += nwarps) {
-      int64_t rbase;
-      if constexpr (D == 2) {
-        rbase = (int64_t)slots[r] * g.n[1];
-      } else {
-        int a = r / H1, b = r - a * H1;
-        rbase = ((int64_t)slots[a] * g.n[1] + slots[H0 + b]) * g.n[2];
-      }
-      for (int c = lane; c < HL; c += 32) {
-        C v = halo[r * HL + c];
-        if (v.x != (R)0 || v.y != (R)0) {
-          C* dst = grid + rbase + sl[c];
-          atomicAdd(&dst->x, v.x);
-          atomicAdd(&dst->y, v.y);
-        }
-      }
-    }
+    bulk_red_add<R>(gp + row0, halo + (size_t)r * HS, (unsigned)(HS * sizeof(C)));
   }
+  bulk_commit_wait_read();
 }
 
 // ================================================================ launchers
-static size_t halo_cells(const Geom& g) {
-  size_t h = 1;
-  for (int i = 0; i < g.d; ++i) h *= g.H[i];
-  return h;
-}
-
-static size_t slot_bytes(const Geom& g) {
-  int s = 0;
-  for (int i = 0; i < g.d; ++i) s += g.H[i];
-  return (s * sizeof(int) + 15) & ~(size_t)15;
+static size_t halo_bytes(const Geom& g, int elem_bytes) {
+  size_t rows = 1;
+  for (int i = 0; i < g.d - 1; ++i) rows *= g.H[i];
+  return ((rows * g.HS * elem_bytes) + 15) & ~(size_t)15;
 }
 
 size_t interp_smem(const Geom& g, int elem_bytes, int threads) {
   (void)threads;
-  size_t off = (halo_cells(g) * elem_bytes + 15) & ~(size_t)15;
-  off += 16 + slot_bytes(g);
-  off += 2 * batch_bytes_of(g.d, INTERP_NB, 2 * g.m + 1, elem_bytes);
-  return off;
+  return halo_bytes(g, elem_bytes) + 16 + 2 * batch_bytes_of(g.d, INTERP_NB, 2 * g.m + 1, elem_bytes);
 }
 
-size_t spread_smem(const Geom& g, int elem_bytes) {
-  size_t off = (halo_cells(g) * elem_bytes + 15) & ~(size_t)15;
-  off += slot_bytes(g);
-  off += 2 * batch_bytes_of(g.d, SPREAD_NB, 2 * g.m + 1, elem_bytes);
-  return off;
+size_t spread_smem_nb(const Geom& g, int elem_bytes, int nb) {
+  const int K = 2 * g.m + 1, WF = 2 * g.m;
+  auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
+  size_t s = halo_bytes(g, elem_bytes) + al((size_t)nb * K * elem_bytes);
+  if (g.d == 3) s += al((size_t)nb * WF * WF * sizeof(double));
+  return s + 2 * batch_bytes_of(g.d, nb, K, elem_bytes);
 }
+
+size_t spread_smem(const Geom& g, int elem_bytes) { return spread_smem_nb(g, elem_bytes, g.nb_spread); }
 
 int spread_threads(const Geom& g) {
-  // d=3: one warp per owned a-row class (2m warps); d=2: 2m half-warp units;
-  // d=1: 64 threads
+  // d=3: one warp per owned a-row class (2m warps); d=1, 2: one warp
   if (g.d == 3) return 32 * std::max(2, std::min(16, 2 * g.m));
-  if (g.d == 2) return 16 * std::max(4, std::min(32, 2 * g.m));
-  return 64;
+  return 32;
 }
 
 template <typename R, int D, int MM>
-static void interp_go(const void* grid, void* f, void*, const double* xs, const int* perm,
-                      const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+static void interp_go(const CUtensorMap* tm, const void* gp, void* f, void*, const double* xs,
+                      const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   const int threads = g.nt_interp;
   size_t smem = interp_smem(g, sizeof(cplx_t<R>), threads);
   auto kern = k_interp<R, D, MM>;
   NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nsubs, threads, smem, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)f, xs, perm, subs, g);
+  kern<<<nsubs, threads, smem, s>>>(*tm, (const cplx_t<R>*)gp, (cplx_t<R>*)f, xs, perm, subs, g);
   count_launch();
 }
 
 template <typename R, int D, int MM>
-static void spread_go(void* grid, const void* f, void* fs, const double* xs, const int* perm,
-                      const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, const double* xs,
+                      const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   const int threads = spread_threads(g);
   size_t smem = spread_smem(g, sizeof(cplx_t<R>));
   auto kern = k_spread<R, D, MM>;
@@ -647,7 +633,7 @@ static void spread_go(void* grid, const void* f, void* fs, const double* xs, con
   k_permute_samples<cplx_t<R>><<<(unsigned)std::min<int64_t>((g.M + 255) / 256, 148 * 64), 256, 0, s>>>(
       (const cplx_t<R>*)f, perm, g.M, (cplx_t<R>*)fs);
   count_launch();
-  kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)grid, (const cplx_t<R>*)fs, xs, subs, g);
+  kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, g);
   count_launch();
 }
 
@@ -671,18 +657,20 @@ static void spread_go(void* grid, const void* f, void* fs, const double* xs, con
     else { NFFTK_DISPATCH_M(FN, R, 3, __VA_ARGS__) }                   \
   } while (0)
 
-void launch_interp(bool single, const void* grid, void* f, const double* xs, const int* perm,
-                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  if (nsubs <= 0) return;
-  if (single) NFFTK_DISPATCH_DM(interp_go, float, grid, f, nullptr, xs, perm, subs, nsubs, g, s);
-  else NFFTK_DISPATCH_DM(interp_go, double, grid, f, nullptr, xs, perm, subs, nsubs, g, s);
-}
-
-void launch_spread(bool single, void* grid, const void* f, void* fs, const double* xs,
+void launch_interp(bool single, const void* tmap, const void* gp, void* f, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
-  if (single) NFFTK_DISPATCH_DM(spread_go, float, grid, f, fs, xs, perm, subs, nsubs, g, s);
-  else NFFTK_DISPATCH_DM(spread_go, double, grid, f, fs, xs, perm, subs, nsubs, g, s);
+  const CUtensorMap* tm = (const CUtensorMap*)tmap;
+  if (single) NFFTK_DISPATCH_DM(interp_go, float, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);
+  else NFFTK_DISPATCH_DM(interp_go, double, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);
+}
+
+void launch_spread(bool single, void* gp, const void* f, void* fs, const double* xs,
+                   const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+  if (nsubs <= 0) return;
+  const CUtensorMap* tm = nullptr;
+  if (single) NFFTK_DISPATCH_DM(spread_go, float, tm, gp, f, fs, xs, perm, subs, nsubs, g, s);
+  else NFFTK_DISPATCH_DM(spread_go, double, tm, gp, f, fs, xs, perm, subs, nsubs, g, s);
 }
 
 }  // namespace nfftk

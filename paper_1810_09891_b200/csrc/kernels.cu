@@ -9,6 +9,8 @@
 // Reference loops these replace: kernels.py:56-416, transform.py:39-176.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -408,5 +410,109 @@ double measure_fma_tflops(bool fp64) {
   cudaEventDestroy(b);
   cudaFree(out);
   return best;
+}
+}  // namespace nfftk
+
+namespace nfftk {
+// ----------------------------------------------- ghost-padded grid copies
+// The padded grid holds cell slot s of the n-grid at padded index s + m and
+// periodic images in the ghost layers, so every tile halo [t T - m, t T + T
+// + m] is one contiguous box at padded origin t T.
+
+// dense -> padded (after the forward FFT): every padded cell reads its image
+__device__ __forceinline__ int wrap_slot(int p, int m, int n) {
+  int s = p - m;  // the padded extent keeps p - m in [-n, 2n) (plan.cu)
+  if (s < 0) s += n;
+  if (s >= n) s -= n;
+  return s;
+}
+
+template <typename C>
+__global__ void k_pad(const C* __restrict__ g0, C* __restrict__ gp, PadGeom q) {
+  const int dl = q.d - 1;
+  const int line = blockIdx.x;
+  int src = 0, rem = line;
+  int lead[MAX_D];
+  for (int i = dl - 1; i >= 0; --i) { lead[i] = rem % q.np[i]; rem /= q.np[i]; }
+  for (int i = 0; i < dl; ++i) src = src * q.n[i] + wrap_slot(lead[i], q.m, q.n[i]);
+  const C* in = g0 + (int64_t)src * q.n[dl];
+  C* out = gp + (int64_t)line * q.np[dl];
+  for (int p = blockIdx.y * blockDim.x + threadIdx.x; p < q.np[dl]; p += gridDim.y * blockDim.x)
+    out[p] = in[wrap_slot(p, q.m, q.n[dl])];
+}
+
+// padded -> dense (after the spread): each dense cell sums its images
+template <typename C>
+__global__ void k_fold(const C* __restrict__ gp, C* __restrict__ g0, PadGeom q) {
+  const int dl = q.d - 1;
+  const int line = blockIdx.x;
+  int rem = line;
+  int c[MAX_D];
+  for (int i = dl - 1; i >= 0; --i) { c[i] = rem % q.n[i]; rem /= q.n[i]; }
+  // padded lines holding images of this dense line (<= 3 per leading dim)
+  int64_t plines[9];
+  int np_lines = 1;
+  plines[0] = 0;
+  for (int i = 0; i < dl; ++i) {
+    int cand[3], nc = 0;
+    for (int k = -1; k <= 1; ++k) {
+      int p = c[i] + q.m + k * q.n[i];
+      if (p >= 0 && p < q.np[i]) cand[nc++] = p;
+    }
+    int cur = np_lines;
+    int64_t tmp[9];
+    int nt = 0;
+    for (int a = 0; a < cur; ++a)
+      for (int b = 0; b < nc && nt < 9; ++b) tmp[nt++] = plines[a] * q.np[i] + cand[b];
+    for (int a = 0; a < nt; ++a) plines[a] = tmp[a];
+    np_lines = nt;
+  }
+  C* out = g0 + (int64_t)line * q.n[dl];
+  const int nl = q.n[dl], npl = q.np[dl];
+  for (int s = blockIdx.y * blockDim.x + threadIdx.x; s < nl; s += gridDim.y * blockDim.x) {
+    double re = 0, im = 0;
+    const int p0 = s + q.m;
+    const bool lo_img = p0 - nl >= 0, hi_img = p0 + nl < npl;
+    for (int a = 0; a < np_lines; ++a) {
+      const C* row = gp + plines[a] * npl;
+      C v = row[p0];
+      re += (double)v.x;
+      im += (double)v.y;
+      if (lo_img) {
+        v = row[p0 - nl];
+        re += (double)v.x;
+        im += (double)v.y;
+      }
+      if (hi_img) {
+        v = row[p0 + nl];
+        re += (double)v.x;
+        im += (double)v.y;
+      }
+    }
+    C v;
+    v.x = (decltype(v.x))re;
+    v.y = (decltype(v.y))im;
+    out[s] = v;
+  }
+}
+
+void launch_pad(bool single, const void* g0, void* gp, const PadGeom& q, cudaStream_t s) {
+  int64_t lines = 1;
+  for (int i = 0; i < q.d - 1; ++i) lines *= q.np[i];
+  int nl = q.np[q.d - 1];
+  dim3 grd((unsigned)lines, (unsigned)std::min(65535, (nl + 255) / 256));
+  if (single) k_pad<float2><<<grd, 256, 0, s>>>((const float2*)g0, (float2*)gp, q);
+  else k_pad<double2><<<grd, 256, 0, s>>>((const double2*)g0, (double2*)gp, q);
+  count_launch();
+}
+
+void launch_fold(bool single, const void* gp, void* g0, const PadGeom& q, cudaStream_t s) {
+  int64_t lines = 1;
+  for (int i = 0; i < q.d - 1; ++i) lines *= q.n[i];
+  int nl = q.n[q.d - 1];
+  dim3 grd((unsigned)lines, (unsigned)std::min(65535, (nl + 255) / 256));
+  if (single) k_fold<float2><<<grd, 256, 0, s>>>((const float2*)gp, (float2*)g0, q);
+  else k_fold<double2><<<grd, 256, 0, s>>>((const double2*)gp, (double2*)g0, q);
+  count_launch();
 }
 }  // namespace nfftk

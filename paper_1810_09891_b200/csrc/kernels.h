@@ -8,6 +8,13 @@
 
 namespace nfftk {
 
+struct PadGeom {
+  int d;
+  int n[MAX_D];
+  int np[MAX_D];
+  int m;
+};
+
 struct DeconvGeomH {
   int d;
   int N[MAX_D];
@@ -31,8 +38,11 @@ void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaSt
 
 void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH& q, cudaStream_t s);
 void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& q, cudaStream_t s);
-void launch_interp(bool single, const void* grid, void* f, const double* xs, const int* perm,
-                   const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+void launch_interp(bool single, const void* tmap, const void* gp, void* f, const double* xs,
+                   const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+void launch_pad(bool single, const void* g0, void* gp, const PadGeom& q, cudaStream_t s);
+void launch_fold(bool single, const void* gp, void* g0, const PadGeom& q, cudaStream_t s);
+size_t spread_smem_nb(const Geom& g, int elem_bytes, int nb);
 void launch_spread(bool single, void* grid, const void* f, void* fs, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
 

@@ -8,6 +8,9 @@
 #include <cstring>
 #include <sstream>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "plan.h"
 
 namespace nfftk {
@@ -114,6 +117,7 @@ Plan::~Plan() {
   cudaFree(lut);
   cudaFree(cols);
   if (!grid_external) cudaFree(grid);
+  cudaFree(gp);
   cudaFree(fhat_dev);
   cudaFree(f_dev);
   cudaFree(f_sorted);
@@ -153,16 +157,27 @@ static void choose_tiles(Plan* p) {
         if (halo_bytes(c) <= 190 * KB) { T = c; break; }
     if (!T) T = 2;
   } else if (p->d == 2) {
-    for (int c : {128, 64, 32, 16, 8, 4, 2})
-      if (halo_bytes(c) <= 100 * KB) { T = c; break; }
+    // single-warp spread CTAs keep a private halo: small tiles
+    for (int c : {16, 8, 4, 2})
+      if (halo_bytes(c) <= 24 * KB) { T = c; break; }
     if (!T) T = 2;
   } else {
-    for (int c = 4096; c >= 2; c /= 2)
-      if (halo_bytes(c) <= 64 * KB) { T = c; break; }
+    for (int c = 512; c >= 2; c /= 2)
+      if (halo_bytes(c) <= 16 * KB) { T = c; break; }
     if (!T) T = 2;
   }
   int force = env_int("NFFTK_TILE", 0);
   if (force > 0) T = force;
+  // the padded extent must keep every padded index within one period of the
+  // grid on either side (pad / fold wrap with one correction)
+  auto fits = [&](int t) {
+    for (int i = 0; i < p->d; ++i) {
+      int ti = std::min(t, p->n[i]), nt = (p->n[i] + ti - 1) / ti;
+      if (nt * ti + p->m + 2 > 2 * p->n[i]) return false;
+    }
+    return true;
+  };
+  while (T > 2 && !fits(T)) T /= 2;
   p->ntiles = 1;
   for (int i = 0; i < p->d; ++i) {
     g.T[i] = std::min(T, p->n[i]);
@@ -170,6 +185,13 @@ static void choose_tiles(Plan* p) {
     g.ntile[i] = (p->n[i] + g.T[i] - 1) / g.T[i];
     p->ntiles *= g.ntile[i];
   }
+  // ghost-padded grid: pad m on the left, >= m+2 on the right (even length)
+  for (int i = 0; i < p->d; ++i) {
+    g.np[i] = g.ntile[i] * g.T[i] + 2 * p->m + 2;
+  }
+  g.HS = g.H[p->d - 1] + (eb == 8 ? 1 : 0);   // complex64 rows padded to 16-byte multiples
+  g.nb_spread = 32;
+  while (g.nb_spread > 4 && spread_smem_nb(g, (int)eb, g.nb_spread) > 220 * KB) g.nb_spread /= 2;
   g.nt_interp = interp_smem(g, (int)eb, 256) > 110 * KB ? 512 : 256;
   g.nt_interp = env_int("NFFTK_INTERP_THREADS", g.nt_interp);
   p->maxsub = env_int("NFFTK_MAXSUB", 1024);
@@ -416,8 +438,52 @@ void plan_set_nodes_device(Plan* p, const double* x, int64_t len, cudaStream_t s
 }
 
 // ------------------------------------------------------------- precompute
+static void build_tensor_map(Plan* p) {
+  const Geom& g = p->geom;
+  if (p->d == 1) { p->tmap_ready = true; return; }   // d = 1 uses a 1-D bulk copy
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    NFFTK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !encode) fail(EK_CUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  // complex128 = two FLOAT64 along the innermost dim; complex64 = one 8-byte element
+  const int scale = p->single ? 1 : 2;
+  const size_t eb = p->elem_bytes();
+  cuuint64_t dims[3];
+  cuuint64_t strides[2];
+  cuuint32_t box[3], estr[3] = {1, 1, 1};
+  int r = p->d;
+  for (int i = 0; i < r; ++i) {
+    dims[i] = (cuuint64_t)g.np[r - 1 - i];
+    box[i] = (cuuint32_t)(i == 0 ? g.HS : g.H[r - 1 - i]);
+  }
+  dims[0] *= scale;
+  box[0] *= scale;
+  strides[0] = (cuuint64_t)g.np[r - 1] * eb;
+  if (r == 3) strides[1] = (cuuint64_t)g.np[2] * g.np[1] * eb;
+  CUresult res = encode((CUtensorMap*)p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)r, p->gp, dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) fail(EK_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
+  p->tmap_ready = true;
+}
+
 static void ensure_grid(Plan* p) {
   if (!p->grid) NFFTK_CUDA(cudaMalloc(&p->grid, p->elem_bytes() * p->grid_size));
+  if (!p->gp) {
+    size_t cells = 1;
+    for (int i = 0; i < p->d; ++i) cells *= (size_t)p->geom.np[i];
+    p->gp_bytes = cells * p->elem_bytes();
+    NFFTK_CUDA(cudaMalloc(&p->gp, p->gp_bytes));
+    p->pq.d = p->d;
+    p->pq.m = p->m;
+    for (int i = 0; i < p->d; ++i) {
+      p->pq.n[i] = p->n[i];
+      p->pq.np[i] = p->geom.np[i];
+    }
+  }
+  if (!p->tmap_ready) build_tensor_map(p);
   if (!p->fft_ready) {
     int nn[MAX_D];
     for (int i = 0; i < p->d; ++i) nn[i] = p->n[i];
@@ -521,8 +587,9 @@ void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
   NFFTK_CUDA(cudaSetDevice(p->device));
   { PhaseScope ps(p, PH_DECONV, s); launch_deconv(p->single, fhat, p->grid, p->dq, s); }
   { PhaseScope ps(p, PH_FFT_FWD, s); exec_fft(p, CUFFT_FORWARD, s); }
+  { PhaseScope ps(p, PH_PAD, s); launch_pad(p->single, p->grid, p->gp, p->pq, s); }
   { PhaseScope ps(p, PH_INTERP, s);
-    launch_interp(p->single, p->grid, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+    launch_interp(p->single, p->tmap, p->gp, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }
@@ -530,11 +597,11 @@ void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
 void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
-  { PhaseScope ps(p, PH_ZERO, s);
-    NFFTK_CUDA(cudaMemsetAsync(p->grid, 0, p->elem_bytes() * p->grid_size, s)); }
+  { PhaseScope ps(p, PH_ZERO, s); NFFTK_CUDA(cudaMemsetAsync(p->gp, 0, p->gp_bytes, s)); }
   { PhaseScope ps(p, PH_SPREAD, s);
     if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * p->M));
-    launch_spread(p->single, p->grid, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+    launch_spread(p->single, p->gp, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+  { PhaseScope ps(p, PH_FOLD, s); launch_fold(p->single, p->gp, p->grid, p->pq, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }

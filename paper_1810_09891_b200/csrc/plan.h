@@ -17,7 +17,7 @@ namespace nfftk {
 
 enum Phase : int {
   PH_DECONV = 0, PH_FFT_FWD, PH_INTERP, PH_ZERO, PH_SPREAD, PH_FFT_INV, PH_PACK,
-  PH_H2D, PH_D2H, PH_COUNT
+  PH_H2D, PH_D2H, PH_PAD, PH_FOLD, PH_COUNT
 };
 
 struct Plan {
@@ -55,8 +55,13 @@ struct Plan {
   double* psi = nullptr;
   double* lut = nullptr;
   double* cols = nullptr;
-  void* grid = nullptr;
+  void* grid = nullptr;              // dense n-grid (cuFFT, deconvolution)
   bool grid_external = false;
+  void* gp = nullptr;                // ghost-padded grid (gridding kernels)
+  size_t gp_bytes = 0;
+  PadGeom pq{};
+  alignas(64) unsigned char tmap[128];  // CUtensorMap of gp (halo boxes)
+  bool tmap_ready = false;
   void* fhat_dev = nullptr;
   void* f_dev = nullptr;
   void* f_sorted = nullptr;         // spread input in tile-sorted order
