@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -584,6 +585,170 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   bulk_commit_wait_read();
 }
 
+// ============================================ B^H, d = 3: register-resident
+// Each thread owns one full halo row (a, b): all H2 = T2 + 2m + 1 cells of it
+// live in registers.  A node's c-offset h2 (and its stencil rows) are the
+// same for every thread, so the c-run of a node is added with a switch on
+// h2 whose bodies index the register row statically -- no shared-memory
+// read-modify-write, no ownership bookkeeping, no conflicts (each cell has
+// exactly one owner).  A warp skips nodes whose stencil misses all its rows.
+// Zero-padded K = 2m+1 factor rows make grid-aligned nodes (width 2m+1) take
+// the same path.  At the end the rows go through shared memory and are
+// added to the padded grid by TMA bulk reductions.
+template <int MM, int T2>
+struct RRThreads {
+  static constexpr int value = (((T2 + 2 * MM + 1) * (T2 + 2 * MM + 1)) + 31) / 32 * 32;
+};
+
+template <typename R, int MM, int T2>
+__global__ void __launch_bounds__(RRThreads<MM, T2>::value, 1)
+k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
+            const double* __restrict__ xs, const int4* __restrict__ subs, Geom g) {
+  using C = cplx_t<R>;
+  constexpr int K = 2 * MM + 1;
+  constexpr int H2 = T2 + 2 * MM + 1;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int NB = g.nb_spread;
+  const int H1 = g.H[1];
+  const int HS = g.HS;
+  const int rows = g.H[0] * H1;
+  size_t off = 0;
+  C* stage = reinterpret_cast<C*>(smem);  // final rows for the bulk reductions
+  off += a16((size_t)rows * HS * sizeof(C));
+  C* coef = reinterpret_cast<C*>(smem + off);  // [NB][K]  f * w0[t]
+  off += a16((size_t)NB * K * sizeof(C));
+  unsigned char* bufbase = smem + off;
+  const size_t bb = batch_bytes_of(3, NB, K, sizeof(C));
+  const int4 sp = subs[blockIdx.x];
+  int tc[3];
+  tile_of<3>(g, sp.x, tc);
+  const int end = sp.y + sp.z;
+  issue_batch<C, 3>(g, xs, nullptr, fsorted, sp.y, min(NB, sp.z), NB, batch_at<C, 3>(bufbase, NB, K));
+  cp_async_commit();
+  const int row = threadIdx.x;
+  const bool owner = row < rows;
+  const int a = owner ? row / H1 : 0, b = owner ? row - (row / H1) * H1 : 0;
+  // rows of this warp: [wr0, wr1] in row-major (a, b) order
+  const int wr0 = min((int)(threadIdx.x & ~31u), rows - 1), wr1 = min((int)(threadIdx.x | 31u), rows - 1);
+  const int wa0 = wr0 / H1, wb0 = wr0 - wa0 * H1, wa1 = wr1 / H1, wb1 = wr1 - wa1 * H1;
+  const int lane = threadIdx.x & 31;
+  R accr[H2], acci[H2];
+#pragma unroll
+  for (int c = 0; c < H2; ++c) accr[c] = acci[c] = 0;
+  bool touched = false;
+  int k = 0;
+  for (int base = sp.y; base < end; base += NB, ++k) {
+    const int nb = min(NB, end - base);
+    const Batch<C, 3> cur = batch_at<C, 3>(bufbase + (k & 1) * bb, NB, K);
+    cp_async_wait_all();
+    __syncthreads();
+    finish_batch<C, 3>(g, tc, nb, NB, 1, cur);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nb * K; q += blockDim.x) {
+      int j = q / K, t = q - j * K;
+      R w0 = (R)cur.w[j * 3 * K + t];
+      C f = cur.fv[j];
+      C c;
+      c.x = f.x * w0;
+      c.y = f.y * w0;
+      coef[q] = c;
+    }
+    __syncthreads();
+    if (base + NB < end) {
+      issue_batch<C, 3>(g, xs, nullptr, fsorted, base + NB, min(NB, end - base - NB), NB,
+                        batch_at<C, 3>(bufbase + ((k + 1) & 1) * bb, NB, K));
+      cp_async_commit();
+    }
+    // which nodes of the batch touch this warp's rows: lane j tests node j
+    unsigned mask = 0;
+    for (int j0 = 0; j0 < nb; j0 += 32) {
+      bool hit = false;
+      const int j = j0 + lane;
+      if (j < nb) {
+        const int* q = cur.hw + j * 8;
+        const int alo = max(q[0], wa0), ahi = min(q[0] + q[3] - 1, wa1);
+        if (alo <= ahi) {
+          // b-range of row a within the warp: full rows between wa0 and wa1
+          const int blo_first = alo == wa0 ? wb0 : 0, bhi_first = alo == wa1 ? wb1 : H1 - 1;
+          const int blo_last = ahi == wa0 ? wb0 : 0, bhi_last = ahi == wa1 ? wb1 : H1 - 1;
+          const int nlo = q[1], nhi = q[1] + q[4] - 1;
+          hit = (max(nlo, blo_first) <= min(nhi, bhi_first)) || (max(nlo, blo_last) <= min(nhi, bhi_last)) ||
+                (ahi - alo >= 2 && nlo <= nhi);
+        }
+      }
+      mask = __ballot_sync(0xffffffffu, hit);
+      while (mask) {
+        const int jb = j0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int* q = cur.hw + jb * 8;
+        const int4 qa = *reinterpret_cast<const int4*>(q);       // h0, h1, h2, W0
+        const int W1 = q[4];
+        const int ta = a - qa.x, tb = b - qa.y;
+        const bool act = owner && ta >= 0 && ta < qa.w && tb >= 0 && tb < W1;
+        const double* w = cur.w + jb * 3 * K;
+        R cr = 0, ci = 0;
+        if (act) {
+          const C cf = coef[jb * K + ta];
+          R w1 = (R)w[K + tb];
+          cr = cf.x * w1;
+          ci = cf.y * w1;
+          touched = true;
+        }
+        R w2[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) w2[t] = (R)w[2 * K + t];
+        switch (qa.z) {
+#define NFFTK_RR_CASE(H)                                           \
+  case H:                                                          \
+    if constexpr (H + K <= H2) {                                   \
+      _Pragma("unroll") for (int t = 0; t < K; ++t) {              \
+        accr[H + t] = fma(cr, w2[t], accr[H + t]);                 \
+        acci[H + t] = fma(ci, w2[t], acci[H + t]);                 \
+      }                                                            \
+    }                                                              \
+    break;
+          NFFTK_RR_CASE(0) NFFTK_RR_CASE(1) NFFTK_RR_CASE(2) NFFTK_RR_CASE(3) NFFTK_RR_CASE(4)
+          NFFTK_RR_CASE(5) NFFTK_RR_CASE(6) NFFTK_RR_CASE(7) NFFTK_RR_CASE(8)
+#undef NFFTK_RR_CASE
+          default: break;
+        }
+      }
+    }
+  }
+  // ---- flush: rows -> shared memory -> TMA bulk reductions into the padded grid
+  if (owner) {
+    C* dst = stage + (size_t)row * HS;
+#pragma unroll
+    for (int c = 0; c < H2; ++c) {
+      C v;
+      v.x = accr[c];
+      v.y = acci[c];
+      dst[c] = v;
+    }
+    if (HS > H2) {
+      C z;
+      z.x = 0;
+      z.y = 0;
+      dst[H2] = z;
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (owner && touched) {
+    int64_t row0 = ((int64_t)(tc[0] * g.T[0] + a) * g.np[1] + tc[1] * g.T[1] + b) * g.np[2] + tc[2] * g.T[2];
+    bulk_red_add<R>(gp + row0, stage + (size_t)row * HS, (unsigned)(HS * sizeof(C)));
+  }
+  bulk_commit_wait_read();
+}
+
+size_t spread_rr_smem(const Geom& g, int elem_bytes) {
+  const int K = 2 * g.m + 1;
+  auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
+  size_t rows = (size_t)g.H[0] * g.H[1];
+  return al(rows * g.HS * elem_bytes) + al((size_t)g.nb_spread * K * elem_bytes) +
+         2 * batch_bytes_of(3, g.nb_spread, K, elem_bytes);
+}
+
 // ================================================================ launchers
 static size_t halo_bytes(const Geom& g, int elem_bytes) {
   size_t rows = 1;
@@ -623,16 +788,33 @@ static void interp_go(const CUtensorMap* tm, const void* gp, void* f, void*, con
   count_launch();
 }
 
+bool spread_rr_ok(const Geom& g, int elem_bytes) {
+  return g.d == 3 && g.m >= 1 && g.m <= 8 && g.T[0] == 8 && g.T[1] == 8 && g.T[2] == 8 &&
+         g.H[0] * g.H[1] <= 512 &&
+         spread_rr_smem(g, elem_bytes) <= 220 * 1024 && !getenv("NFFTK_NO_RR");
+}
+
 template <typename R, int D, int MM>
 static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, const double* xs,
                       const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+  k_permute_samples<cplx_t<R>><<<(unsigned)std::min<int64_t>((g.M + 255) / 256, 148 * 64), 256, 0, s>>>(
+      (const cplx_t<R>*)f, perm, g.M, (cplx_t<R>*)fs);
+  count_launch();
+  if constexpr (D == 3 && MM > 0) {
+    if (spread_rr_ok(g, sizeof(cplx_t<R>))) {
+      const int threads = (g.H[0] * g.H[1] + 31) & ~31;
+      size_t smem = spread_rr_smem(g, sizeof(cplx_t<R>));
+      auto kern = k_spread_rr<R, MM, 8>;
+      NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, g);
+      count_launch();
+      return;
+    }
+  }
   const int threads = spread_threads(g);
   size_t smem = spread_smem(g, sizeof(cplx_t<R>));
   auto kern = k_spread<R, D, MM>;
   NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_permute_samples<cplx_t<R>><<<(unsigned)std::min<int64_t>((g.M + 255) / 256, 148 * 64), 256, 0, s>>>(
-      (const cplx_t<R>*)f, perm, g.M, (cplx_t<R>*)fs);
-  count_launch();
   kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, g);
   count_launch();
 }

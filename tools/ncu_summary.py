@@ -77,5 +77,8 @@ if __name__ == "__main__":
     raw(rep)
     if len(sys.argv) > 2:
         nodes = float(sys.argv[2])
-        for k in ("k_interp", "k_spread"):
-            mix(rep, k, nodes)
+        for k in (sys.argv[3:] or ["k_interp", "k_spread"]):
+            try:
+                mix(rep, k, nodes)
+            except (IndexError, ValueError):
+                pass
