@@ -460,12 +460,13 @@ void oracle_node_order(int d, const int *n, int64_t M, const double *x, int64_t 
     free(r);
 }
 
-/* transform.py:121-176 -- f_hat = D^H F^H B^H f.
- * blockwise != 0 restates the slab-owned parallel adjoint (kernels.py:293-401,
- * transform.py:144-158); otherwise the sequential natural-order spread
- * (transform.py:159-171). nthreads <= 0 uses the OpenMP default. */
-int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
-                   const double *x, const cplx *f, cplx *fhat, int blockwise, int nthreads) {
+/* transform.py:121-171 -- B^H only: the oversampled grid after spreading
+ * (before the FFT).  blockwise != 0 restates the slab-owned parallel adjoint
+ * (kernels.py:293-401, transform.py:144-158); otherwise the sequential
+ * natural-order spread (transform.py:159-171).  nthreads <= 0 uses the
+ * OpenMP default. */
+int oracle_spread_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                       const double *x, const cplx *f, cplx *g, int blockwise, int nthreads) {
     oplan p;
     if (setup(&p, d, N, n, m, code, mode)) return -1;
 #ifdef _OPENMP
@@ -473,8 +474,8 @@ int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode,
 #else
     nthreads = 1;
 #endif
-    int64_t G = grid_total(&p), K = freq_total(&p);
-    cplx *g = (cplx *)calloc((size_t)G, sizeof(cplx));
+    int64_t G = grid_total(&p);
+    memset(g, 0, sizeof(cplx) * (size_t)G);
     if (blockwise && nthreads > 1) {
         int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)M);
         oracle_node_order(d, n, M, x, order);
@@ -502,6 +503,15 @@ int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode,
     } else {
         for (int64_t j = 0; j < M; ++j) spread_node(&p, x, j, f[j], g, 0, 0, 0);
     }
+    free(p.lut);
+    return 0;
+}
+
+/* transform.py:174-176 -- F^H (sign +1) and D^H of a spread grid (in place) */
+int oracle_adjoint_finish(int d, const int *N, const int *n, int m, int code, cplx *g, cplx *fhat) {
+    oplan p;
+    if (setup(&p, d, N, n, m, code, MODE_DIRECT)) return -1;
+    int64_t G = grid_total(&p), K = freq_total(&p);
     oracle_fft_nd(d, n, g, +1);
     double **cols = deconv_cols(&p);
     double gs = (double)G;
@@ -511,9 +521,20 @@ int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode,
         fhat[lin] = deconv_value(&p, cols, g[slot], kk, gs);
     }
     free_cols(&p, cols);
-    free(g);
-    free(p.lut);
     return 0;
+}
+
+/* transform.py:121-176 -- f_hat = D^H F^H B^H f */
+int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                   const double *x, const cplx *f, cplx *fhat, int blockwise, int nthreads) {
+    if (d < 1 || d > 3) return -1;
+    int64_t G = 1;
+    for (int i = 0; i < d; ++i) G *= n[i];
+    cplx *g = (cplx *)malloc(sizeof(cplx) * (size_t)G);
+    int rc = oracle_spread_grid(d, N, n, m, code, mode, M, x, f, g, blockwise, nthreads);
+    if (!rc) rc = oracle_adjoint_finish(d, N, n, m, code, g, fhat);
+    free(g);
+    return rc;
 }
 
 /* transform.py:188-203 -- exact forward sums sum_k f_hat_k e^{-2 pi i k.x_j} */

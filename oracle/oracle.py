@@ -41,6 +41,11 @@ def lib():
         L.oracle_adjoint.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int,
                                      ctypes.c_int]
+        L.oracle_spread_grid.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int,
+                                         ctypes.c_int]
+        L.oracle_adjoint_finish.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
+                                            vp, vp]
         L.oracle_ndft.argtypes = [ctypes.c_int, i32p, ctypes.c_int64, vp, vp, vp]
         L.oracle_ndft_adjoint.argtypes = [ctypes.c_int, i32p, ctypes.c_int64, vp, vp, vp]
         L.oracle_fft_nd.argtypes = [ctypes.c_int, i32p, vp, ctypes.c_int]
@@ -100,6 +105,32 @@ def adjoint(N, n, m, x, f, window="kaiserbessel", lut=False, blockwise=None, thr
                               int(bool(blockwise)), int(threads))
     if rc:
         raise ValueError("oracle_adjoint supports d <= 3")
+    return out
+
+
+def spread_grid(N, n, m, x, f, window="kaiserbessel", lut=False, blockwise=None, threads=0):
+    """B^H only (transform.py:121-171): the spread n-grid before the FFT."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    M, d = x.shape
+    if blockwise is None:
+        blockwise = d > 1
+    f = np.ascontiguousarray(f, dtype=np.complex128).ravel()
+    g = np.empty(int(np.prod(n)), dtype=np.complex128)
+    rc = lib().oracle_spread_grid(d, _ivec(N), _ivec(n), int(m), _kind(window),
+                                  MODE_LUT if lut else MODE_DIRECT, M, _ptr(x), _ptr(f), _ptr(g),
+                                  int(bool(blockwise)), int(threads))
+    if rc:
+        raise ValueError("oracle_spread_grid supports d <= 3")
+    return g
+
+
+def adjoint_finish(N, n, m, grid, window="kaiserbessel"):
+    """F^H + D^H of a spread grid (transform.py:174-176)."""
+    g = np.array(grid, dtype=np.complex128, copy=True).ravel()
+    out = np.empty(int(np.prod(N)), dtype=np.complex128)
+    rc = lib().oracle_adjoint_finish(len(N), _ivec(N), _ivec(n), int(m), _kind(window), _ptr(g), _ptr(out))
+    if rc:
+        raise ValueError("oracle_adjoint_finish supports d <= 3")
     return out
 
 

@@ -6,35 +6,90 @@ Design:
              own GPU (replicated, no communication) and interpolates only its
              node shard.  Samples stay sharded.
 * adjoint -- every rank spreads its node shard into a private full n-grid,
-             the grids are summed with one NCCL all-reduce over NVLink, then
-             every rank runs F^H and D^H (replicated result).
+             the grids are summed with one all-reduce (NCCL over NVLink on
+             B200), then every rank runs F^H and D^H (replicated result).
 
-The all-reduce is the only data-path collective; it is the real exchange
-step of the adjoint (sum over all nodes).  ``torch.distributed`` supplies
-the plumbing; the grid is a torch tensor bound into the plan
-(``nfftk_bind_grid``) so the collective reduces the library's grid in place.
+The all-reduce is the only data-path collective; it is the real exchange step
+of the adjoint (a sum over all nodes).  ``torch.distributed`` supplies the
+plumbing.  The orchestration below is engine-agnostic: ``GpuEngine`` runs the
+CUDA library (the grid is a torch tensor bound into the plan with
+``nfftk_bind_grid`` so the collective reduces the library's grid in place);
+tests drive the same ``DistributedNfft`` with a CPU engine over gloo.
 """
 
 import torch
 import torch.distributed as dist
 
-from .plan import Plan
+
+def shard_bounds(M_total, world, rank):
+    """Contiguous node range [lo, hi) of ``rank`` (balanced to within one node)."""
+    lo = (M_total * rank) // world
+    hi = (M_total * (rank + 1)) // world
+    return lo, hi
 
 
-class DistributedPlan:
-    """A plan over this rank's node shard plus the grid reduction."""
+class DistributedNfft:
+    """Node-sharded trafo / adjoint over a process group.
 
-    def __init__(self, N, M_local, n=None, m=None, f1=None, f2=None, window="kaiserbessel",
-                 precision="double", group=None, device=None):
+    ``engine`` provides: ``trafo(fhat) -> f_local``, ``spread(f_local) -> grid``
+    (a tensor the collective may reduce in place) and ``finish(grid) -> fhat``.
+    """
+
+    def __init__(self, engine, group=None):
+        self.engine = engine
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def trafo(self, fhat):
+        """Samples at this rank's nodes (no communication)."""
+        return self.engine.trafo(fhat)
+
+    def adjoint(self, f_local):
+        """Full coefficient vector, identical on every rank."""
+        grid = self.engine.spread(f_local)
+        if self.world > 1:
+            dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=self.group)
+        return self.engine.finish(grid)
+
+
+class GpuEngine:
+    """The CUDA library as a DistributedNfft engine (one Plan per rank)."""
+
+    def __init__(self, plan, device):
+        self.plan = plan
+        real = torch.float32 if plan.single else torch.float64
+        # dense n-grid as interleaved reals: the collective reduces a plain buffer
+        self.grid = torch.empty(2 * plan.grid_size, dtype=real, device=device)
+        plan.bind_grid(self.grid)
+        self._out = None
+
+    def trafo(self, fhat, out=None):
+        return self.plan.trafo(fhat, out=out)
+
+    def spread(self, f_local):
+        self.plan.spread(f_local)
+        return self.grid
+
+    def finish(self, grid, out=None):
+        assert grid.data_ptr() == self.grid.data_ptr()
+        if out is None:
+            cdt = torch.complex64 if self.plan.single else torch.complex128
+            out = torch.empty(self.plan.num_freqs, dtype=cdt, device=self.grid.device)
+        return self.plan.adjoint_finish(out)
+
+
+class DistributedPlan(DistributedNfft):
+    """Convenience: a CUDA plan over this rank's node shard plus the reduction."""
+
+    def __init__(self, N, M_local, n=None, m=None, f1=None, f2=None, window="kaiserbessel",
+                 precision="double", group=None, device=None):
+        from .plan import Plan
+
+        device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.plan = Plan(N, M_local, n=n, m=m, f1=f1, f2=f2, window=window, precision=precision)
-        real = torch.float32 if self.plan.single else torch.float64
-        # grid as interleaved reals: NCCL reduces it as a plain float buffer
-        self.grid = torch.empty(2 * self.plan.grid_size, dtype=real, device=self.device)
-        self.plan.bind_grid(self.grid)
+        self.device = device
+        super().__init__(GpuEngine(self.plan, device), group)
 
     @property
     def M_local(self):
@@ -46,25 +101,11 @@ class DistributedPlan:
     def precompute(self):
         self.plan.precompute()
 
-    def trafo(self, fhat):
-        """Sharded samples of this rank's nodes (no communication)."""
-        return self.plan.trafo(fhat)
-
     def adjoint(self, f_local, out=None):
-        """Full coefficient vector, identical on every rank."""
-        self.plan.spread(f_local)
+        grid = self.engine.spread(f_local)
         if self.world > 1:
-            dist.all_reduce(self.grid, op=dist.ReduceOp.SUM, group=self.group)
-        if out is None:
-            out = torch.empty(self.plan.num_freqs, dtype=f_local.dtype, device=f_local.device)
-        return self.plan.adjoint_finish(out)
+            dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=self.group)
+        return self.engine.finish(grid, out=out)
 
     def close(self):
         self.plan.close()
-
-
-def shard_bounds(M_total, world, rank):
-    """Contiguous node range of ``rank`` (balanced to within one node)."""
-    lo = (M_total * rank) // world
-    hi = (M_total * (rank + 1)) // world
-    return lo, hi

@@ -357,3 +357,20 @@ def test_full_size_trafo_subsample_and_adjoint_identity(cfg, oracle, torch):
     rhs = torch.vdot(a, fh_d).item()
     scale = torch.linalg.norm(fh_d).item() * torch.linalg.norm(g).item()
     assert abs(lhs - rhs) / scale < 1e-12
+
+
+def test_distributed_plan_single_rank_matches_plan(torch):
+    """GPU engine of the node-sharded orchestration (world = 1): bound grid,
+    spread, finish reproduce Plan.adjoint / trafo."""
+    from paper_1810_09891_b200.distributed import DistributedPlan
+
+    c = case("d3_m6")
+    dev = torch.device("cuda", 0)
+    dp = DistributedPlan(tuple(c["N"]), c["x"].shape[0], n=tuple(c["n"]), m=int(c["m"]), device=dev)
+    dp.set_nodes(torch.from_numpy(c["x"]).to(dev))
+    dp.precompute()
+    f = dp.trafo(torch.from_numpy(c["fhat"]).to(dev)).cpu().numpy()
+    a = dp.adjoint(torch.from_numpy(c["f"]).to(dev)).cpu().numpy()
+    assert e2(c["trafo"], f) < TOL128
+    assert e2(c["adjoint"], a) < TOL128
+    dp.close()
