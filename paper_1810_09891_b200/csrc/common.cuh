@@ -122,6 +122,7 @@ struct Geom {
   int np[MAX_D];          // ghost-padded grid (periodic images, halo = one box)
   int HS;                 // halo row stride (elements) of the last dim
   int nb_spread;          // spread node batch size
+  int debug;              // NFFTK_DEBUG bits (experiments only; 0 in production)
 };
 
 // -------------------------------------------------------- device window

@@ -603,7 +603,7 @@ struct RRThreads {
 template <typename R, int MM, int T2>
 __global__ void __launch_bounds__(RRThreads<MM, T2>::value, 1)
 k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
-            const double* __restrict__ xs, const int4* __restrict__ subs, Geom g) {
+            const double* __restrict__ xs, const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
   constexpr int K = 2 * MM + 1;
   constexpr int H2 = T2 + 2 * MM + 1;
@@ -613,37 +613,50 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   const int HS = g.HS;
   const int rows = g.H[0] * H1;
   size_t off = 0;
-  C* stage = reinterpret_cast<C*>(smem);  // final rows for the bulk reductions
+  C* stage = reinterpret_cast<C*>(smem);  // per-thread staging rows for the bulk reductions
   off += a16((size_t)rows * HS * sizeof(C));
   C* coef = reinterpret_cast<C*>(smem + off);  // [NB][K]  f * w0[t]
   off += a16((size_t)NB * K * sizeof(C));
   unsigned char* bufbase = smem + off;
   const size_t bb = batch_bytes_of(3, NB, K, sizeof(C));
-  const int4 sp = subs[blockIdx.x];
+  int s = blockIdx.x;
+  if (s >= nsubs) return;
+  int4 sp = subs[s];
   int tc[3];
   tile_of<3>(g, sp.x, tc);
-  const int end = sp.y + sp.z;
   issue_batch<C, 3>(g, xs, nullptr, fsorted, sp.y, min(NB, sp.z), NB, batch_at<C, 3>(bufbase, NB, K));
   cp_async_commit();
-  const int row = threadIdx.x;
+  // strided row ownership: warp w, lane l owns halo row l * nw + w, so every
+  // warp holds a mix of centre rows (hit by most nodes) and edge rows (hit by
+  // few) -- equal work per warp, no batch-barrier imbalance
+  const int nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int row = lane * nw + (threadIdx.x >> 5);
   const bool owner = row < rows;
   const int a = owner ? row / H1 : 0, b = owner ? row - (row / H1) * H1 : 0;
-  // rows of this warp: [wr0, wr1] in row-major (a, b) order
-  const int wr0 = min((int)(threadIdx.x & ~31u), rows - 1), wr1 = min((int)(threadIdx.x | 31u), rows - 1);
-  const int wa0 = wr0 / H1, wb0 = wr0 - wa0 * H1, wa1 = wr1 / H1, wb1 = wr1 - wa1 * H1;
-  const int lane = threadIdx.x & 31;
   R accr[H2], acci[H2];
 #pragma unroll
   for (int c = 0; c < H2; ++c) accr[c] = acci[c] = 0;
   bool touched = false;
-  int k = 0;
-  for (int base = sp.y; base < end; base += NB, ++k) {
+  int base = sp.y;
+  for (int k = 0;; ++k) {
+    const int end = sp.y + sp.z;
     const int nb = min(NB, end - base);
     const Batch<C, 3> cur = batch_at<C, 3>(bufbase + (k & 1) * bb, NB, K);
+    // next (subproblem, batch) item of this persistent CTA
+    int s_n = s, base_n = base + NB;
+    int4 sp_n = sp;
+    if (base_n >= end) {
+      s_n = s + gridDim.x;
+      if (s_n < nsubs) {
+        sp_n = subs[s_n];
+        base_n = sp_n.y;
+      }
+    }
     cp_async_wait_all();
     __syncthreads();
     finish_batch<C, 3>(g, tc, nb, NB, 1, cur);
-    __syncthreads();
+    if (g.mode != MODE_TENSOR) __syncthreads();  // computed factors feed the coefficients
     for (int q = threadIdx.x; q < nb * K; q += blockDim.x) {
       int j = q / K, t = q - j * K;
       R w0 = (R)cur.w[j * 3 * K + t];
@@ -654,34 +667,15 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       coef[q] = c;
     }
     __syncthreads();
-    if (base + NB < end) {
-      issue_batch<C, 3>(g, xs, nullptr, fsorted, base + NB, min(NB, end - base - NB), NB,
+    if (s_n < nsubs) {
+      issue_batch<C, 3>(g, xs, nullptr, fsorted, base_n, min(NB, sp_n.y + sp_n.z - base_n), NB,
                         batch_at<C, 3>(bufbase + ((k + 1) & 1) * bb, NB, K));
       cp_async_commit();
     }
-    // which nodes of the batch touch this warp's rows: lane j tests node j
-    unsigned mask = 0;
-    for (int j0 = 0; j0 < nb; j0 += 32) {
-      bool hit = false;
-      const int j = j0 + lane;
-      if (j < nb) {
-        const int* q = cur.hw + j * 8;
-        const int alo = max(q[0], wa0), ahi = min(q[0] + q[3] - 1, wa1);
-        if (alo <= ahi) {
-          // b-range of row a within the warp: full rows between wa0 and wa1
-          const int blo_first = alo == wa0 ? wb0 : 0, bhi_first = alo == wa1 ? wb1 : H1 - 1;
-          const int blo_last = ahi == wa0 ? wb0 : 0, bhi_last = ahi == wa1 ? wb1 : H1 - 1;
-          const int nlo = q[1], nhi = q[1] + q[4] - 1;
-          hit = (max(nlo, blo_first) <= min(nhi, bhi_first)) || (max(nlo, blo_last) <= min(nhi, bhi_last)) ||
-                (ahi - alo >= 2 && nlo <= nhi);
-        }
-      }
-      mask = __ballot_sync(0xffffffffu, hit);
-      while (mask) {
-        const int jb = j0 + __ffs(mask) - 1;
-        mask &= mask - 1;
+    if (!(g.debug & 2)) {
+      for (int jb = 0; jb < nb; ++jb) {
         const int* q = cur.hw + jb * 8;
-        const int4 qa = *reinterpret_cast<const int4*>(q);       // h0, h1, h2, W0
+        const int4 qa = *reinterpret_cast<const int4*>(q);  // h0, h1, h2, W0
         const int W1 = q[4];
         const int ta = a - qa.x, tb = b - qa.y;
         const bool act = owner && ta >= 0 && ta < qa.w && tb >= 0 && tb < W1;
@@ -714,31 +708,43 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
         }
       }
     }
-  }
-  // ---- flush: rows -> shared memory -> TMA bulk reductions into the padded grid
-  if (owner) {
-    C* dst = stage + (size_t)row * HS;
+    if (s_n != s) {
+      // tile done: each thread stages and bulk-reduces its own row -- no CTA
+      // barrier; the row slot is reused only after this thread's previous
+      // reduction finished reading it
+      if (owner && touched && !(g.debug & 1)) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        C* dst = stage + (size_t)row * HS;
 #pragma unroll
-    for (int c = 0; c < H2; ++c) {
-      C v;
-      v.x = accr[c];
-      v.y = acci[c];
-      dst[c] = v;
+        for (int c = 0; c < H2; ++c) {
+          C v;
+          v.x = accr[c];
+          v.y = acci[c];
+          dst[c] = v;
+        }
+        if (HS > H2) {
+          C z;
+          z.x = 0;
+          z.y = 0;
+          dst[H2] = z;
+        }
+        fence_proxy_async_smem();
+        int64_t row0 =
+            ((int64_t)(tc[0] * g.T[0] + a) * g.np[1] + tc[1] * g.T[1] + b) * g.np[2] + tc[2] * g.T[2];
+        bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+        asm volatile("cp.async.bulk.commit_group;\n" ::);
+      }
+#pragma unroll
+      for (int c = 0; c < H2; ++c) accr[c] = acci[c] = 0;
+      touched = false;
+      if (s_n >= nsubs) break;
+      s = s_n;
+      sp = sp_n;
+      tile_of<3>(g, sp.x, tc);
     }
-    if (HS > H2) {
-      C z;
-      z.x = 0;
-      z.y = 0;
-      dst[H2] = z;
-    }
+    base = base_n;
   }
-  fence_proxy_async_smem();
-  __syncthreads();
-  if (owner && touched) {
-    int64_t row0 = ((int64_t)(tc[0] * g.T[0] + a) * g.np[1] + tc[1] * g.T[1] + b) * g.np[2] + tc[2] * g.T[2];
-    bulk_red_add<R>(gp + row0, stage + (size_t)row * HS, (unsigned)(HS * sizeof(C)));
-  }
-  bulk_commit_wait_read();
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
 size_t spread_rr_smem(const Geom& g, int elem_bytes) {
@@ -806,7 +812,17 @@ static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, con
       size_t smem = spread_rr_smem(g, sizeof(cplx_t<R>));
       auto kern = k_spread_rr<R, MM, 8>;
       NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<nsubs, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, g);
+      // persistent CTAs: as many as fit on the device at once
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        NFFTK_CUDA(cudaGetDevice(&dev));
+        NFFTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      int per_sm = 0;
+      NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+      int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
+      kern<<<grid, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, nsubs, g);
       count_launch();
       return;
     }

@@ -195,6 +195,7 @@ static void choose_tiles(Plan* p) {
   g.nt_interp = interp_smem(g, (int)eb, 256) > 110 * KB ? 512 : 256;
   g.nt_interp = env_int("NFFTK_INTERP_THREADS", g.nt_interp);
   p->maxsub = env_int("NFFTK_MAXSUB", 1024);
+  g.debug = env_int("NFFTK_DEBUG", 0);
 }
 
 static void fill_geom(Plan* p) {
