@@ -241,94 +241,103 @@ void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaSt
 }
 
 // ------------------------------------------------------------ D and D^H
-// transform.py:57-63 + :96-97: g[k mod n] = f_hat_k / |I_n| / phi_hat_0 /
-// ... / phi_hat_{d-1} (division order kept), zero elsewhere.  One block row
-// per grid line along the last dim (blockIdx.x = line, blockIdx.y = chunk).
+// transform.py:57-63 + :96-97: g[k mod n] = f_hat_k / (|I_n| prod_i phi_hat_i)
+// and zero elsewhere; transform.py:174-176 applies the same scaling to the
+// packed g.  The reciprocal factors are tabulated at precompute; the
+// product 1/|I_n| * prod 1/phi_hat differs from the reference's sequence of
+// divisions only in the last bits (~4 ulp).  One warp per grid line (lanes
+// along the contiguous last dim), eight lines per 256-thread block.
 struct DeconvGeom {
   int d;
   int N[MAX_D];
   int n[MAX_D];
-  const double* col[MAX_D];  // phi_hat (times wscale) over k + N/2
-  double grid_size;
+  const double* icol[MAX_D];  // 1 / (phi_hat * wscale) over k + N/2
+  double inv_gs;              // 1 / |I_n|
 };
 
 template <typename R>
-__global__ void k_deconv_pad(const cplx_t<R>* __restrict__ fhat, cplx_t<R>* __restrict__ grid,
-                             DeconvGeom q) {
+__global__ void __launch_bounds__(256) k_deconv_pad(const cplx_t<R>* __restrict__ fhat,
+                                                    cplx_t<R>* __restrict__ grid, DeconvGeom q,
+                                                    int64_t lines) {
+  using C = cplx_t<R>;
   const int dl = q.d - 1;
-  const int nl = q.n[dl], Nl = q.N[dl];
-  int64_t line = blockIdx.x;
-  // decode the line's leading slots (dims 0..d-2), last dim slot from threads
-  int kidx[MAX_D];
-  bool inside = true;
-  int64_t fl = 0, rem = line;
-  int lead[MAX_D];
-  for (int i = dl - 1; i >= 0; --i) { lead[i] = (int)(rem % q.n[i]); rem /= q.n[i]; }
-  for (int i = 0; i < dl; ++i) {
-    int sl = lead[i], Ni = q.N[i];
-    int k = sl < Ni / 2 ? sl + Ni / 2 : (sl >= q.n[i] - Ni / 2 ? sl - q.n[i] + Ni / 2 : -1);
-    if (k < 0) inside = false;
-    kidx[i] = k;
-    fl = fl * Ni + (k < 0 ? 0 : k);
-  }
-  cplx_t<R>* out = grid + line * nl;
-  for (int sl = blockIdx.y * blockDim.x + threadIdx.x; sl < nl; sl += gridDim.y * blockDim.x) {
-    cplx_t<R> v;
-    v.x = 0;
-    v.y = 0;
-    int k = sl < Nl / 2 ? sl + Nl / 2 : (sl >= nl - Nl / 2 ? sl - nl + Nl / 2 : -1);
-    if (inside && k >= 0) {
-      cplx_t<R> a = fhat[fl * Nl + k];
-      double re = (double)a.x / q.grid_size, im = (double)a.y / q.grid_size;
-      for (int i = 0; i < dl; ++i) { double c = q.col[i][kidx[i]]; re /= c; im /= c; }
-      double c = q.col[dl][k];
-      re /= c;
-      im /= c;
-      v.x = (R)re;
-      v.y = (R)im;
+  const int nl = q.n[dl], Nl = q.N[dl], h = Nl / 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t line = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+    bool inside = true;
+    int64_t fl = 0, rem = line;
+    double fac = q.inv_gs;
+    int lead[MAX_D];
+    for (int i = dl - 1; i >= 0; --i) { lead[i] = (int)(rem % q.n[i]); rem /= q.n[i]; }
+    for (int i = 0; i < dl; ++i) {
+      int sl = lead[i], Ni = q.N[i];
+      int k = sl < Ni / 2 ? sl + Ni / 2 : (sl >= q.n[i] - Ni / 2 ? sl - q.n[i] + Ni / 2 : -1);
+      inside = inside && k >= 0;
+      fl = fl * Ni + (k < 0 ? 0 : k);
+      if (k >= 0) fac *= q.icol[i][k];
     }
-    out[sl] = v;
+    C* out = grid + line * nl;
+    const C* in = fhat + fl * Nl;
+    for (int sl = lane; sl < nl; sl += 32) {
+      C v;
+      v.x = 0;
+      v.y = 0;
+      int k = sl < h ? sl + h : (sl >= nl - h ? sl - nl + h : -1);
+      if (inside && k >= 0) {
+        C a = in[k];
+        double f = fac * q.icol[dl][k];
+        v.x = (R)((double)a.x * f);
+        v.y = (R)((double)a.y * f);
+      }
+      out[sl] = v;
+    }
   }
 }
 
-// transform.py:174-176: f_hat_k = g[k mod n] / |I_n| / prod phi_hat.
 template <typename R>
-__global__ void k_pack_deconv(const cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ fhat,
-                              DeconvGeom q) {
+__global__ void __launch_bounds__(256) k_pack_deconv(const cplx_t<R>* __restrict__ grid,
+                                                     cplx_t<R>* __restrict__ fhat, DeconvGeom q,
+                                                     int64_t lines) {
+  using C = cplx_t<R>;
   const int dl = q.d - 1;
   const int nl = q.n[dl], Nl = q.N[dl];
-  int64_t line = blockIdx.x;  // line over N_0..N_{d-2}
-  int kidx[MAX_D];
-  int64_t gl = 0, rem = line;
-  for (int i = dl - 1; i >= 0; --i) { kidx[i] = (int)(rem % q.N[i]); rem /= q.N[i]; }
-  for (int i = 0; i < dl; ++i) {
-    int k = kidx[i] - q.N[i] / 2;
-    int sl = k < 0 ? k + q.n[i] : k;
-    gl = gl * q.n[i] + sl;
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t line = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+    int64_t gl = 0, rem = line;
+    double fac = q.inv_gs;
+    int kidx[MAX_D];
+    for (int i = dl - 1; i >= 0; --i) { kidx[i] = (int)(rem % q.N[i]); rem /= q.N[i]; }
+    for (int i = 0; i < dl; ++i) {
+      int k = kidx[i] - q.N[i] / 2;
+      gl = gl * q.n[i] + (k < 0 ? k + q.n[i] : k);
+      fac *= q.icol[i][kidx[i]];
+    }
+    const C* in = grid + gl * nl;
+    C* out = fhat + line * Nl;
+    for (int kl = lane; kl < Nl; kl += 32) {
+      int k = kl - Nl / 2;
+      C a = in[k < 0 ? k + nl : k];
+      double f = fac * q.icol[dl][kl];
+      C v;
+      v.x = (R)((double)a.x * f);
+      v.y = (R)((double)a.y * f);
+      out[kl] = v;
+    }
   }
-  for (int kl = blockIdx.y * blockDim.x + threadIdx.x; kl < Nl; kl += gridDim.y * blockDim.x) {
-    int k = kl - Nl / 2;
-    int sl = k < 0 ? k + nl : k;
-    cplx_t<R> a = grid[gl * nl + sl];
-    double re = (double)a.x / q.grid_size, im = (double)a.y / q.grid_size;
-    for (int i = 0; i < dl; ++i) { double c = q.col[i][kidx[i]]; re /= c; im /= c; }
-    double c = q.col[dl][kl];
-    re /= c;
-    im /= c;
-    cplx_t<R> v;
-    v.x = (R)re;
-    v.y = (R)im;
-    fhat[line * Nl + kl] = v;
-  }
+}
+
+static unsigned line_blocks(int64_t lines) {
+  int64_t b = (lines + 7) / 8;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 16));
 }
 
 template <typename R>
 void launch_deconv_pad(const void* fhat, void* grid, const DeconvGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.n[i];
-  int nl = q.n[q.d - 1];
-  dim3 grd((unsigned)lines, (unsigned)((nl + 255) / 256 > 65535 ? 65535 : (nl + 255) / 256));
-  k_deconv_pad<R><<<grd, 256, 0, s>>>((const cplx_t<R>*)fhat, (cplx_t<R>*)grid, q);
+  k_deconv_pad<R><<<line_blocks(lines), 256, 0, s>>>((const cplx_t<R>*)fhat, (cplx_t<R>*)grid, q, lines);
   count_launch();
 }
 
@@ -336,18 +345,15 @@ template <typename R>
 void launch_pack_deconv(const void* grid, void* fhat, const DeconvGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.N[i];
-  int Nl = q.N[q.d - 1];
-  dim3 grd((unsigned)lines, (unsigned)((Nl + 255) / 256 > 65535 ? 65535 : (Nl + 255) / 256));
-  k_pack_deconv<R><<<grd, 256, 0, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)fhat, q);
+  k_pack_deconv<R><<<line_blocks(lines), 256, 0, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)fhat, q, lines);
   count_launch();
 }
-
 
 void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH& qh, cudaStream_t s) {
   DeconvGeom q;
   q.d = qh.d;
-  for (int i = 0; i < MAX_D; ++i) { q.N[i] = qh.N[i]; q.n[i] = qh.n[i]; q.col[i] = qh.col[i]; }
-  q.grid_size = qh.grid_size;
+  for (int i = 0; i < MAX_D; ++i) { q.N[i] = qh.N[i]; q.n[i] = qh.n[i]; q.icol[i] = qh.icol[i]; }
+  q.inv_gs = 1.0 / qh.grid_size;
   if (single) launch_deconv_pad<float>(fhat, grid, q, s);
   else launch_deconv_pad<double>(fhat, grid, q, s);
 }
@@ -355,8 +361,8 @@ void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH&
 void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& qh, cudaStream_t s) {
   DeconvGeom q;
   q.d = qh.d;
-  for (int i = 0; i < MAX_D; ++i) { q.N[i] = qh.N[i]; q.n[i] = qh.n[i]; q.col[i] = qh.col[i]; }
-  q.grid_size = qh.grid_size;
+  for (int i = 0; i < MAX_D; ++i) { q.N[i] = qh.N[i]; q.n[i] = qh.n[i]; q.icol[i] = qh.icol[i]; }
+  q.inv_gs = 1.0 / qh.grid_size;
   if (single) launch_pack_deconv<float>(grid, fhat, q, s);
   else launch_pack_deconv<double>(grid, fhat, q, s);
 }
@@ -428,91 +434,94 @@ __device__ __forceinline__ int wrap_slot(int p, int m, int n) {
 }
 
 template <typename C>
-__global__ void k_pad(const C* __restrict__ g0, C* __restrict__ gp, PadGeom q) {
+__global__ void __launch_bounds__(256) k_pad(const C* __restrict__ g0, C* __restrict__ gp, PadGeom q,
+                                             int lines) {
   const int dl = q.d - 1;
-  const int line = blockIdx.x;
-  int src = 0, rem = line;
-  int lead[MAX_D];
-  for (int i = dl - 1; i >= 0; --i) { lead[i] = rem % q.np[i]; rem /= q.np[i]; }
-  for (int i = 0; i < dl; ++i) src = src * q.n[i] + wrap_slot(lead[i], q.m, q.n[i]);
-  const C* in = g0 + (int64_t)src * q.n[dl];
-  C* out = gp + (int64_t)line * q.np[dl];
-  for (int p = blockIdx.y * blockDim.x + threadIdx.x; p < q.np[dl]; p += gridDim.y * blockDim.x)
-    out[p] = in[wrap_slot(p, q.m, q.n[dl])];
+  const int nl = q.n[dl], npl = q.np[dl];
+  const int lane = threadIdx.x & 31;
+  const int wstride = (gridDim.x * blockDim.x) >> 5;
+  for (int line = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+    int src = 0, rem = line;
+    int lead[MAX_D];
+    for (int i = dl - 1; i >= 0; --i) { lead[i] = rem % q.np[i]; rem /= q.np[i]; }
+    for (int i = 0; i < dl; ++i) src = src * q.n[i] + wrap_slot(lead[i], q.m, q.n[i]);
+    const C* in = g0 + (int64_t)src * nl;
+    C* out = gp + (int64_t)line * npl;
+    for (int p = lane; p < npl; p += 32) out[p] = in[wrap_slot(p, q.m, nl)];
+  }
 }
 
 // padded -> dense (after the spread): each dense cell sums its images
 template <typename C>
-__global__ void k_fold(const C* __restrict__ gp, C* __restrict__ g0, PadGeom q) {
+__global__ void __launch_bounds__(256) k_fold(const C* __restrict__ gp, C* __restrict__ g0, PadGeom q,
+                                              int lines) {
   const int dl = q.d - 1;
-  const int line = blockIdx.x;
-  int rem = line;
-  int c[MAX_D];
-  for (int i = dl - 1; i >= 0; --i) { c[i] = rem % q.n[i]; rem /= q.n[i]; }
-  // padded lines holding images of this dense line (<= 3 per leading dim)
-  int64_t plines[9];
-  int np_lines = 1;
-  plines[0] = 0;
-  for (int i = 0; i < dl; ++i) {
-    int cand[3], nc = 0;
-    for (int k = -1; k <= 1; ++k) {
-      int p = c[i] + q.m + k * q.n[i];
-      if (p >= 0 && p < q.np[i]) cand[nc++] = p;
-    }
-    int cur = np_lines;
-    int64_t tmp[9];
-    int nt = 0;
-    for (int a = 0; a < cur; ++a)
-      for (int b = 0; b < nc && nt < 9; ++b) tmp[nt++] = plines[a] * q.np[i] + cand[b];
-    for (int a = 0; a < nt; ++a) plines[a] = tmp[a];
-    np_lines = nt;
-  }
-  C* out = g0 + (int64_t)line * q.n[dl];
   const int nl = q.n[dl], npl = q.np[dl];
-  for (int s = blockIdx.y * blockDim.x + threadIdx.x; s < nl; s += gridDim.y * blockDim.x) {
-    double re = 0, im = 0;
-    const int p0 = s + q.m;
-    const bool lo_img = p0 - nl >= 0, hi_img = p0 + nl < npl;
-    for (int a = 0; a < np_lines; ++a) {
-      const C* row = gp + plines[a] * npl;
-      C v = row[p0];
-      re += (double)v.x;
-      im += (double)v.y;
-      if (lo_img) {
-        v = row[p0 - nl];
-        re += (double)v.x;
-        im += (double)v.y;
+  const int lane = threadIdx.x & 31;
+  const int wstride = (gridDim.x * blockDim.x) >> 5;
+  for (int line = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+    int rem = line;
+    int c[MAX_D];
+    for (int i = dl - 1; i >= 0; --i) { c[i] = rem % q.n[i]; rem /= q.n[i]; }
+    // padded lines holding images of this dense line (<= 3 per leading dim)
+    int64_t plines[9];
+    int np_lines = 1;
+    plines[0] = 0;
+    for (int i = 0; i < dl; ++i) {
+      int cand[3], nc = 0;
+      for (int k = -1; k <= 1; ++k) {
+        int p = c[i] + q.m + k * q.n[i];
+        if (p >= 0 && p < q.np[i]) cand[nc++] = p;
       }
-      if (hi_img) {
-        v = row[p0 + nl];
-        re += (double)v.x;
-        im += (double)v.y;
-      }
+      int64_t tmp[9];
+      int nt = 0;
+      for (int a2 = 0; a2 < np_lines; ++a2)
+        for (int b2 = 0; b2 < nc && nt < 9; ++b2) tmp[nt++] = plines[a2] * q.np[i] + cand[b2];
+      for (int a2 = 0; a2 < nt; ++a2) plines[a2] = tmp[a2];
+      np_lines = nt;
     }
-    C v;
-    v.x = (decltype(v.x))re;
-    v.y = (decltype(v.y))im;
-    out[s] = v;
+    C* out = g0 + (int64_t)line * nl;
+    for (int s2 = lane; s2 < nl; s2 += 32) {
+      double re = 0, im = 0;
+      const int p0 = s2 + q.m;
+      const bool lo_img = p0 - nl >= 0, hi_img = p0 + nl < npl;
+      for (int a2 = 0; a2 < np_lines; ++a2) {
+        const C* row = gp + plines[a2] * npl;
+        C v = row[p0];
+        re += (double)v.x;
+        im += (double)v.y;
+        if (lo_img) {
+          v = row[p0 - nl];
+          re += (double)v.x;
+          im += (double)v.y;
+        }
+        if (hi_img) {
+          v = row[p0 + nl];
+          re += (double)v.x;
+          im += (double)v.y;
+        }
+      }
+      C v;
+      v.x = (decltype(v.x))re;
+      v.y = (decltype(v.y))im;
+      out[s2] = v;
+    }
   }
 }
 
 void launch_pad(bool single, const void* g0, void* gp, const PadGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.np[i];
-  int nl = q.np[q.d - 1];
-  dim3 grd((unsigned)lines, (unsigned)std::min(65535, (nl + 255) / 256));
-  if (single) k_pad<float2><<<grd, 256, 0, s>>>((const float2*)g0, (float2*)gp, q);
-  else k_pad<double2><<<grd, 256, 0, s>>>((const double2*)g0, (double2*)gp, q);
+  if (single) k_pad<float2><<<line_blocks(lines), 256, 0, s>>>((const float2*)g0, (float2*)gp, q, (int)lines);
+  else k_pad<double2><<<line_blocks(lines), 256, 0, s>>>((const double2*)g0, (double2*)gp, q, (int)lines);
   count_launch();
 }
 
 void launch_fold(bool single, const void* gp, void* g0, const PadGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.n[i];
-  int nl = q.n[q.d - 1];
-  dim3 grd((unsigned)lines, (unsigned)std::min(65535, (nl + 255) / 256));
-  if (single) k_fold<float2><<<grd, 256, 0, s>>>((const float2*)gp, (float2*)g0, q);
-  else k_fold<double2><<<grd, 256, 0, s>>>((const double2*)gp, (double2*)g0, q);
+  if (single) k_fold<float2><<<line_blocks(lines), 256, 0, s>>>((const float2*)gp, (float2*)g0, q, (int)lines);
+  else k_fold<double2><<<line_blocks(lines), 256, 0, s>>>((const double2*)gp, (double2*)g0, q, (int)lines);
   count_launch();
 }
 }  // namespace nfftk

@@ -19,7 +19,7 @@ struct DeconvGeomH {
   int d;
   int N[MAX_D];
   int n[MAX_D];
-  const double* col[MAX_D];  // device: phi_hat_i(k) * wscale_i for k + N_i/2
+  const double* icol[MAX_D];  // device: 1 / (phi_hat_i(k) * wscale_i) for k + N_i/2
   double grid_size;
 };
 

@@ -511,7 +511,7 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   std::vector<double> cols;
   for (int i = 0; i < p->d; ++i) {
     std::vector<double> t = plan_phi_hut(p, i);
-    for (int k = 0; k < p->N[i]; ++k) cols.push_back(t[k] * p->wscale[i]);
+    for (int k = 0; k < p->N[i]; ++k) cols.push_back(1.0 / (t[k] * p->wscale[i]));
   }
   if (!p->cols) NFFTK_CUDA(cudaMalloc(&p->cols, sizeof(double) * cols.size()));
   NFFTK_CUDA(cudaMemcpyAsync(p->cols, cols.data(), sizeof(double) * cols.size(),
@@ -522,7 +522,7 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   for (int i = 0; i < p->d; ++i) {
     p->dq.N[i] = p->N[i];
     p->dq.n[i] = p->n[i];
-    p->dq.col[i] = p->cols + off;
+    p->dq.icol[i] = p->cols + off;
     off += p->N[i];
   }
   // factor mode precedence PSI > LUT > DIRECT (transform.py:72-80)
