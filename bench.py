@@ -86,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -400,29 +400,57 @@ def ctypes_fma_peaks(_lib):
     return a.value, b.value
 
 
+def ncu_traffic(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` at
+    ``config`` from the committed ncu --set full summary (profiles/*/ncu_traffic.json),
+    or None when no capture exists."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json"))):
+        try:
+            with open(path) as fh:
+                best = json.load(fh).get(config, {}).get(kernel, best)
+        except (OSError, ValueError):
+            pass
+    return best
+
+
 def roofline(w, phases, steps, s, peaks, fma_tflops):
     """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
     M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
-    (4 w^d M flops with w = 2m)."""
-    ti = phases.get("interp", (0.0, 0))
-    ts = phases.get("spread", (0.0, 0))
-    name, (ms, calls) = ("spread", ts) if ts[0] >= ti[0] else ("interp", ti)
-    if not calls:
-        return None
-    per = ms / calls
-    traffic_alg = w.M * (8 * w.d + s + 4) + s * w.grid_size
-    achieved = traffic_alg / (per * 1e-3) / 1e9
-    flops = 4 * (2 * w.m) ** w.d * w.M
-    tflops = flops / (per * 1e-3) / 1e12
-    return {
-        "kernel": f"k_{name}_tiled", "bound": "hbm", "achieved": achieved,
-        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-        "traffic": None, "algorithmic_bytes_per_launch": traffic_alg,
-        "avg_launch_ms": per, "peak_source": peaks["source"],
-        "fma": {"achieved_tflops": tflops, "peak_tflops": fma_tflops,
-                "frac": tflops / fma_tflops if fma_tflops else None,
-                "flops_per_launch": flops, "peak_source": "k_fma_peak microbenchmark (measured in run)"},
+    (4 w^d M flops with w = 2m).  Times are CUDA-event durations of the kernel
+    launches inside the timed region (library phase events on the launch stream)."""
+    kernels = {
+        "interp": "k_interp",
+        "spread": "k_spread_rr" if (w.d == 3 and w.m <= 8 and min(w.n) >= 8) else "k_spread",
     }
+    out = {}
+    for ph, kname in kernels.items():
+        ms, calls = phases.get(ph, (0.0, 0))
+        if not calls:
+            continue
+        per = ms / calls
+        traffic_alg = w.M * (8 * w.d + s + 4) + s * w.grid_size
+        achieved = traffic_alg / (per * 1e-3) / 1e9
+        flops = 4 * (2 * w.m) ** w.d * w.M
+        tflops = flops / (per * 1e-3) / 1e12
+        out[ph] = {
+            "kernel": kname, "bound": "hbm", "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": ncu_traffic(w.name, kname), "algorithmic_bytes_per_launch": traffic_alg,
+            "avg_launch_ms": per, "peak_source": peaks["source"],
+            "fma": {"achieved_tflops": tflops, "peak_tflops": fma_tflops,
+                    "frac": tflops / fma_tflops if fma_tflops else None,
+                    "flops_per_launch": flops,
+                    "peak_source": "k_fma_peak microbenchmark (measured in run)"},
+        }
+    if not out:
+        return None
+    dom = max(out, key=lambda k: out[k]["avg_launch_ms"])
+    line = dict(out[dom])
+    line["other"] = {k: v for k, v in out.items() if k != dom}
+    return line
 
 
 if __name__ == "__main__":

@@ -64,7 +64,7 @@ SIGNATURES = {
 }
 
 PHASES = ("deconv", "fft_fwd", "interp", "zero", "spread", "fft_inv", "pack", "h2d", "d2h",
-          "pad", "fold")
+          "pad", "fold", "permute")
 
 _lib = None
 

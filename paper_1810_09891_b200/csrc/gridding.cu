@@ -800,12 +800,16 @@ bool spread_rr_ok(const Geom& g, int elem_bytes) {
          spread_rr_smem(g, elem_bytes) <= 220 * 1024 && !getenv("NFFTK_NO_RR");
 }
 
-template <typename R, int D, int MM>
-static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, const double* xs,
-                      const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  k_permute_samples<cplx_t<R>><<<(unsigned)std::min<int64_t>((g.M + 255) / 256, 148 * 64), 256, 0, s>>>(
-      (const cplx_t<R>*)f, perm, g.M, (cplx_t<R>*)fs);
+void launch_permute(bool single, const void* f, const int* perm, int64_t M, void* fs, cudaStream_t s) {
+  unsigned blocks = (unsigned)std::min<int64_t>((M + 255) / 256, 148 * 64);
+  if (single) k_permute_samples<float2><<<blocks, 256, 0, s>>>((const float2*)f, perm, M, (float2*)fs);
+  else k_permute_samples<double2><<<blocks, 256, 0, s>>>((const double2*)f, perm, M, (double2*)fs);
   count_launch();
+}
+
+template <typename R, int D, int MM>
+static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const double* xs,
+                      const int*, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if constexpr (D == 3 && MM > 0) {
     if (spread_rr_ok(g, sizeof(cplx_t<R>))) {
       const int threads = (g.H[0] * g.H[1] + 31) & ~31;

@@ -40,6 +40,7 @@ void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH&
 void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& q, cudaStream_t s);
 void launch_interp(bool single, const void* tmap, const void* gp, void* f, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+void launch_permute(bool single, const void* f, const int* perm, int64_t M, void* fs, cudaStream_t s);
 void launch_pad(bool single, const void* g0, void* gp, const PadGeom& q, cudaStream_t s);
 void launch_fold(bool single, const void* gp, void* g0, const PadGeom& q, cudaStream_t s);
 size_t spread_smem_nb(const Geom& g, int elem_bytes, int nb);

@@ -599,8 +599,9 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
   { PhaseScope ps(p, PH_ZERO, s); NFFTK_CUDA(cudaMemsetAsync(p->gp, 0, p->gp_bytes, s)); }
+  if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * p->M));
+  { PhaseScope ps(p, PH_PERMUTE, s); launch_permute(p->single, f, p->perm, p->M, p->f_sorted, s); }
   { PhaseScope ps(p, PH_SPREAD, s);
-    if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * p->M));
     launch_spread(p->single, p->gp, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
   { PhaseScope ps(p, PH_FOLD, s); launch_fold(p->single, p->gp, p->grid, p->pq, s); }
   NFFTK_CUDA(cudaGetLastError());

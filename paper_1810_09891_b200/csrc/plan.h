@@ -17,7 +17,7 @@ namespace nfftk {
 
 enum Phase : int {
   PH_DECONV = 0, PH_FFT_FWD, PH_INTERP, PH_ZERO, PH_SPREAD, PH_FFT_INV, PH_PACK,
-  PH_H2D, PH_D2H, PH_PAD, PH_FOLD, PH_COUNT
+  PH_H2D, PH_D2H, PH_PAD, PH_FOLD, PH_PERMUTE, PH_COUNT
 };
 
 struct Plan {
