@@ -9,6 +9,7 @@
 // phase timing, multi-GPU grid binding).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -16,6 +17,8 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+
+#include <omp.h>
 
 #include "plan.h"
 
@@ -114,6 +117,22 @@ double* alloc_host(int64_t doubles, bool* pinned) {
   return (double*)ptr;
 }
 
+// Large host copies into the library-owned buffers are split across the host
+// cores (the reference's set_fhat / set_f copy too, cabi.py:149-160).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  if (bytes < (1u << 20)) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const int nt = std::min(16, omp_get_max_threads());
+  const size_t chunk = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
+#pragma omp parallel for num_threads(nt) schedule(static, 1)
+  for (int t = 0; t < nt; ++t) {
+    size_t off = (size_t)t * chunk;
+    if (off < bytes) memcpy((char*)dst + off, (const char*)src + off, std::min(chunk, bytes - off));
+  }
+}
+
 double* fhat_buf(Plan* p) {
   if (!p->fhat_host) p->fhat_host = alloc_host(2 * p->num_freqs, &p->fhat_pinned);
   return p->fhat_host;
@@ -184,7 +203,7 @@ static int32_t set_complex(int32_t h, const double* values, int64_t len, bool fh
       fail(EK_SHAPE, std::string(fhat ? "fhat" : "f") + " needs " + std::to_string(2 * count) +
                          " interleaved doubles, got " + std::to_string(len));
     double* dst = fhat ? fhat_buf(p) : f_buf(p);
-    memcpy(dst, values, sizeof(double) * 2 * count);
+    par_memcpy(dst, values, sizeof(double) * 2 * count);
   });
 }
 
