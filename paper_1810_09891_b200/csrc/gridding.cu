@@ -598,10 +598,12 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
 template <int MM, int T2>
 struct RRThreads {
   static constexpr int value = (((T2 + 2 * MM + 1) * (T2 + 2 * MM + 1)) + 31) / 32 * 32;
+  // CTAs per SM the register budget allows (accumulator rows dominate)
+  static constexpr int blocks = value * 2 * 102 <= 65536 && MM <= 4 ? 2 : 1;
 };
 
 template <typename R, int MM, int T2>
-__global__ void __launch_bounds__(RRThreads<MM, T2>::value, 1)
+__global__ void __launch_bounds__(RRThreads<MM, T2>::value, RRThreads<MM, T2>::blocks)
 k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
             const double* __restrict__ xs, const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
@@ -688,24 +690,36 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
           ci = cf.y * w1;
           touched = true;
         }
-        R w2[K];
-#pragma unroll
-        for (int t = 0; t < K; ++t) w2[t] = (R)w[2 * K + t];
-        switch (qa.z) {
-#define NFFTK_RR_CASE(H)                                           \
+        // c-run factors: preloaded into a register array for small m (latency
+        // off the FMA chain), loaded inside the case for large m (register
+        // pressure at 1 CTA/SM); measured both ways on C3 (m=6) and C5 (m=4)
+#define NFFTK_RR_CASE(H, WT)                                       \
   case H:                                                          \
     if constexpr (H + K <= H2) {                                   \
       _Pragma("unroll") for (int t = 0; t < K; ++t) {              \
-        accr[H + t] = fma(cr, w2[t], accr[H + t]);                 \
-        acci[H + t] = fma(ci, w2[t], acci[H + t]);                 \
+        accr[H + t] = fma(cr, WT, accr[H + t]);                    \
+        acci[H + t] = fma(ci, WT, acci[H + t]);                    \
       }                                                            \
     }                                                              \
     break;
-          NFFTK_RR_CASE(0) NFFTK_RR_CASE(1) NFFTK_RR_CASE(2) NFFTK_RR_CASE(3) NFFTK_RR_CASE(4)
-          NFFTK_RR_CASE(5) NFFTK_RR_CASE(6) NFFTK_RR_CASE(7) NFFTK_RR_CASE(8)
-#undef NFFTK_RR_CASE
-          default: break;
+#define NFFTK_RR_SWITCH(WT)                                                                      \
+  switch (qa.z) {                                                                                \
+    NFFTK_RR_CASE(0, WT) NFFTK_RR_CASE(1, WT) NFFTK_RR_CASE(2, WT) NFFTK_RR_CASE(3, WT)          \
+    NFFTK_RR_CASE(4, WT) NFFTK_RR_CASE(5, WT) NFFTK_RR_CASE(6, WT) NFFTK_RR_CASE(7, WT)          \
+    NFFTK_RR_CASE(8, WT)                                                                         \
+    default: break;                                                                              \
+  }
+        if constexpr (MM <= 4) {
+          R w2[K];
+#pragma unroll
+          for (int t = 0; t < K; ++t) w2[t] = (R)w[2 * K + t];
+          NFFTK_RR_SWITCH(w2[t])
+        } else {
+          const double* w2 = w + 2 * K;
+          NFFTK_RR_SWITCH((R)w2[t])
         }
+#undef NFFTK_RR_SWITCH
+#undef NFFTK_RR_CASE
       }
     }
     if (s_n != s) {
