@@ -116,7 +116,8 @@ struct Geom {
   double wscale[MAX_D];   // window normalisation (1 for c128; 1/phi(0) for c64)
   const double* lut;      // d * (LUT_SIZE+1)  (MODE_LUT)
   double lut_step[MAX_D];
-  const double* psi;      // M * d * (2m+1) in sorted order (MODE_TENSOR)
+  const double* psi;      // M * psi_row(d, 2m+1) in sorted order (MODE_TENSOR)
+  const int4* rec;        // M per-node stencil records, sorted order
   int64_t M;
   int nt_interp;          // threads per interp CTA
   int np[MAX_D];          // ghost-padded grid (periodic images, halo = one box)
@@ -185,6 +186,11 @@ __device__ __forceinline__ double dim_factor(const Geom& g, int dim, double x, i
   if (g.code == WINDOW_KB) return window_kb(off, g.nd[dim], g.md, g.b[dim]);
   return window_gauss(off, g.nd[dim], g.b[dim]);
 }
+
+// PRE_PSI row of one node: d factor vectors of 2m+1, padded to an even count
+// so every node row (and, for d = 3, the last-dim vector) is 16-byte aligned
+// for bulk copies and 128-bit shared loads.
+__host__ __device__ inline int psi_row(int d, int K) { return (d * K + 1) & ~1; }
 
 template <typename R> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };

@@ -85,6 +85,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // TMA: whole halo box of the padded grid -> shared memory
 template <int D>
 __device__ __forceinline__ void tma_load_box(void* sdst, const CUtensorMap* tm, const int* c,
@@ -148,7 +152,7 @@ struct Batch {
 
 __host__ __device__ inline size_t batch_bytes_of(int d, int nb, int K, int elem) {
   auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
-  return al(sizeof(double) * d * nb) + al(sizeof(double) * nb * d * K) +
+  return al(sizeof(double) * d * nb) + al(sizeof(double) * nb * psi_row(d, K)) +
          al(sizeof(int) * nb * (2 * d + 2)) + al(sizeof(int) * nb) + al((size_t)elem * nb);
 }
 
@@ -158,7 +162,7 @@ __device__ __forceinline__ Batch<C, D> batch_at(unsigned char* p, int nb, int K)
   b.x = reinterpret_cast<double*>(p);
   p += a16(sizeof(double) * D * nb);
   b.w = reinterpret_cast<double*>(p);
-  p += a16(sizeof(double) * nb * D * K);
+  p += a16(sizeof(double) * nb * psi_row(D, K));
   b.hw = reinterpret_cast<int*>(p);
   p += a16(sizeof(int) * nb * (2 * D + 2));
   b.pb = reinterpret_cast<int*>(p);
@@ -171,7 +175,7 @@ template <typename C, int D>
 __device__ __forceinline__ void issue_batch(const Geom& g, const double* __restrict__ xs,
                                             const int* __restrict__ perm, const C* __restrict__ fs,
                                             int base, int nb, int NB, const Batch<C, D>& b) {
-  const int K = 2 * g.m + 1, per = D * K;
+  const int K = 2 * g.m + 1, per = psi_row(D, K);
   for (int q = threadIdx.x; q < D * nb; q += blockDim.x) {
     int dim = q / nb, j = q - dim * nb;
     cp_async8(b.x + dim * NB + j, xs + dim * g.M + base + j);
@@ -192,7 +196,7 @@ __device__ __forceinline__ void issue_batch(const Geom& g, const double* __restr
 template <typename C, int D>
 __device__ __forceinline__ void finish_batch(const Geom& g, const int* tc, int nb, int NB, int ua,
                                              const Batch<C, D>& b) {
-  const int K = 2 * g.m + 1, per = D * K;
+  const int K = 2 * g.m + 1, per = psi_row(D, K);
   for (int j = threadIdx.x; j < nb; j += blockDim.x) {
     bool fast = true;
     int* q = b.hw + j * (2 * D + 2);
@@ -210,6 +214,10 @@ __device__ __forceinline__ void finish_batch(const Geom& g, const int* tc, int n
   if (g.mode != MODE_TENSOR) {
     for (int q = threadIdx.x; q < nb * per; q += blockDim.x) {
       int j = q / per, r = q - j * per, dim = r / K, t = r - dim * K;
+      if (dim >= D) {  // row padding
+        b.w[q] = 0.0;
+        continue;
+      }
       double x = b.x[dim * NB + j];
       Stencil st = stencil(x, g.nd[dim], g.md);
       b.w[q] = t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0;
@@ -297,7 +305,7 @@ k_interp(const __grid_constant__ CUtensorMap tmap, const cplx_t<R>* __restrict__
       const int jb = j0 + sub;
       const bool active = jb < nb;
       const int* q = cur.hw + (active ? jb : j0) * (2 * D + 2);
-      const double* w = cur.w + (active ? jb : j0) * D * K;
+      const double* w = cur.w + (active ? jb : j0) * psi_row(D, K);
       R are = 0, aim = 0;
       if (active) {
         if (MM > 0 && q[2 * D]) {
@@ -471,7 +479,7 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     // derived per-node data: row coefficients, factor plane
     for (int q = threadIdx.x; q < nb * K; q += blockDim.x) {
       int j = q / K, t = q - j * K;
-      R w0 = (R)cur.w[j * D * K + t];
+      R w0 = (R)cur.w[j * psi_row(D, K) + t];
       C f = cur.fv[j];
       C c;
       c.x = f.x * w0;
@@ -482,7 +490,7 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       if (MM > 0) {
         for (int q = threadIdx.x; q < nb * WF * WF; q += blockDim.x) {
           int j = q / (WF * WF), p = q - j * (WF * WF), t1 = p / WF, t2 = p - t1 * WF;
-          plane[q] = cur.w[j * D * K + K + t1] * cur.w[j * D * K + 2 * K + t2];
+          plane[q] = cur.w[j * psi_row(D, K) + K + t1] * cur.w[j * psi_row(D, K) + 2 * K + t2];
         }
       }
     }
@@ -516,7 +524,7 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
           }
         } else {
           const int h1 = q[1], h2 = q[2], W0 = q[3], W1 = q[4], W2 = q[5];
-          const double* w = cur.w + jb * D * K;
+          const double* w = cur.w + jb * psi_row(D, K);
           for (int a = h0 + d0; a < h0 + W0; a += UA) {
             const C cf = coef[jb * K + (a - h0)];
             C* pl = halo + (a * H1 + h1) * HS + h2;
@@ -538,7 +546,7 @@ k_spread(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       // lanes over the node's stencil cells (distinct cells, no conflicts)
       for (int jb = 0; jb < nb; ++jb) {
         const int* q = cur.hw + jb * (2 * D + 2);
-        const double* w = cur.w + jb * D * K;
+        const double* w = cur.w + jb * psi_row(D, K);
         if constexpr (D == 2) {
           const int W0 = q[2], W1 = q[3];
           C* corner = halo + q[0] * HS + q[1];
@@ -661,7 +669,7 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     if (g.mode != MODE_TENSOR) __syncthreads();  // computed factors feed the coefficients
     for (int q = threadIdx.x; q < nb * K; q += blockDim.x) {
       int j = q / K, t = q - j * K;
-      R w0 = (R)cur.w[j * 3 * K + t];
+      R w0 = (R)cur.w[j * psi_row(3, K) + t];
       C f = cur.fv[j];
       C c;
       c.x = f.x * w0;
@@ -681,7 +689,7 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
         const int W1 = q[4];
         const int ta = a - qa.x, tb = b - qa.y;
         const bool act = owner && ta >= 0 && ta < qa.w && tb >= 0 && tb < W1;
-        const double* w = cur.w + jb * 3 * K;
+        const double* w = cur.w + jb * psi_row(3, K);
         R cr = 0, ci = 0;
         if (act) {
           const C cf = coef[jb * K + ta];
@@ -761,6 +769,271 @@ k_spread_rr(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
+// ------------------------------------------- C': pipelined register spread
+// PRE_PSI (tensor) mode, d = 3.  Same row ownership and register
+// accumulators as k_spread_rr, fed by a ring of S node-batch stages instead of
+// lock-step batches:
+//  * a stage is three TMA bulk copies (PRE_PSI rows, stencil records, sorted
+//    samples) completing on the stage's `full` mbarrier -- no per-node
+//    coordinate loads, no stencil arithmetic, no CTA barrier;
+//  * each warp releases a stage on its `empty` mbarrier when done; thread 0
+//    refills the stage consumed one step earlier (lag 1), so warps drift
+//    freely within the ring;
+//  * nodes of a tile are sorted by their last-dim stencil start (k_bin_keys),
+//    so the offset switch runs once per run of equal starts, not per node.
+struct StageMeta {
+  int tile;  // tile of this batch
+  int nb;    // nodes (< 0: end of work)
+  int last;  // last batch of its tile: flush after it
+  int foff;  // sample offset inside the stage (alignment of the bulk copy)
+};
+
+__host__ __device__ inline size_t pipe_stage_bytes(int nb, int K, int elem) {
+  auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
+  return al(sizeof(double) * nb * psi_row(3, K)) + al(16 * (size_t)nb) + al((size_t)elem * (nb + 2));
+}
+
+// Compile-time geometry of k_spread_pipe (T = 8 in every dim): halo rows,
+// threads, CTAs per SM, and the largest ring (batch NB x S stages) that fits.
+template <typename R, int MM>
+struct PipeCfg {
+  static constexpr int K = 2 * MM + 1;
+  static constexpr int H = 8 + K;                        // halo edge
+  static constexpr int ELEM = 2 * (int)sizeof(R);        // complex element bytes
+  static constexpr int HS = ELEM == 8 ? H + 1 : H;       // row stride (Geom::HS)
+  static constexpr int ROWS = H * H;
+  static constexpr int THREADS = (ROWS + 31) / 32 * 32;
+  static constexpr int BLOCKS = THREADS * 2 * 102 <= 65536 && MM <= 4 ? 2 : 1;
+  static constexpr int PR = (3 * K + 1) & ~1;
+  static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
+  static constexpr size_t stage_bytes(int nb) {
+    return al(sizeof(double) * nb * PR) + al(16 * (size_t)nb) + al((size_t)ELEM * (nb + 2));
+  }
+  static constexpr size_t rows_bytes = al((size_t)ROWS * HS * ELEM);
+  static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMeta) * s + 32); }
+  static constexpr size_t total(int nb, int s) { return s * stage_bytes(nb) + ctl_bytes(s) + rows_bytes; }
+  static constexpr size_t budget = BLOCKS == 2 ? 112 * 1024 : 224 * 1024;
+  static constexpr int pick_nb() {
+    for (int nb : {32, 16, 8})
+      for (int s : {4, 3, 2})
+        if (total(nb, s) <= budget) return nb;
+    return 0;
+  }
+  static constexpr int pick_s() {
+    for (int nb : {32, 16, 8})
+      for (int s : {4, 3, 2})
+        if (total(nb, s) <= budget) return s;
+    return 0;
+  }
+  static constexpr int NB = pick_nb();
+  static constexpr int S = pick_s();
+  static constexpr size_t SB = stage_bytes(NB > 0 ? NB : 1);
+  static constexpr size_t W_BYTES = al(sizeof(double) * (NB > 0 ? NB : 1) * PR);
+  static constexpr size_t R_BYTES = al(16 * (size_t)(NB > 0 ? NB : 1));
+  static constexpr size_t CTL = (S > 0 ? S : 1) * SB;    // control block offset
+  static constexpr size_t ROWS_OFF = CTL + ctl_bytes(S > 0 ? S : 1);
+  static constexpr size_t SMEM = ROWS_OFF + rows_bytes;
+};
+
+template <typename R, int MM>
+__global__ void __launch_bounds__(PipeCfg<R, MM>::THREADS, PipeCfg<R, MM>::BLOCKS)
+k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
+              const double* __restrict__ psi, const int4* __restrict__ rec,
+              const int4* __restrict__ subs, int nsubs, Geom g) {
+  using C = cplx_t<R>;
+  using P = PipeCfg<R, MM>;
+  constexpr int K = P::K, H2 = P::H, HS = P::HS, PR = P::PR, NB = P::NB, S = P::S;
+  constexpr int KP = (K + 1) / 2;
+  constexpr int FA = 16 / (int)sizeof(C);  // samples per 16 bytes
+  constexpr int NW = P::THREADS / 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  // layout: ring stages | full[S] empty[S] meta[S] producer state | halo rows
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
+  unsigned long long* empty = full + S;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + S);
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k
+  C* stage = reinterpret_cast<C*>(smem + P::ROWS_OFF);  // per-thread staging rows
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NW);
+    }
+    pst[0] = blockIdx.x;
+    pst[4] = 0;
+    if (blockIdx.x < nsubs) {
+      const int4 sp = subs[blockIdx.x];
+      pst[1] = sp.y;
+      pst[2] = sp.y + sp.z;
+      pst[3] = sp.x;
+    }
+  }
+  __syncthreads();
+
+  // ---- producer (thread 0): state in shared memory, so thread 0 keeps no
+  // extra registers live across the node loop
+  auto produce = [&]() {
+    const int pk = pst[4];
+    const int slot = pk % S;
+    if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
+    StageMeta* mt = meta + slot;
+    pst[4] = pk + 1;
+    if (pst[0] >= nsubs) {
+      mt->nb = -1;
+      mbar_arrive(full + slot);
+      return;
+    }
+    const int pbase = pst[1], pend = pst[2];
+    const int nb = min(NB, pend - pbase);
+    const int foff = pbase & (FA - 1);
+    const int fcnt = (nb + foff + FA - 1) & ~(FA - 1);
+    mt->tile = pst[3];
+    mt->nb = nb;
+    mt->last = pbase + nb >= pend;
+    mt->foff = foff;
+    unsigned char* st = smem + slot * P::SB;
+    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb,
+                   fb = (unsigned)sizeof(C) * fcnt;
+    mbar_expect_tx(full + slot, wb + rb + fb);
+    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
+    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (pbase + nb < pend) {
+      pst[1] = pbase + nb;
+    } else {
+      const int s = pst[0] + gridDim.x;
+      pst[0] = s;
+      if (s < nsubs) {
+        const int4 sp = subs[s];
+        pst[1] = sp.y;
+        pst[2] = sp.y + sp.z;
+        pst[3] = sp.x;
+      }
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < S - 1; ++i) produce();
+
+  // strided row ownership (see k_spread_rr); non-owners get an out-of-range
+  // row so the stencil test never passes
+  const int row = lane * NW + (threadIdx.x >> 5);
+  const bool owner = row < P::ROWS;
+  const int a = owner ? row / H2 : -(1 << 20), b = owner ? row % H2 : -(1 << 20);
+  int k = 0;
+  for (;;) {  // tiles of this CTA
+    R accr[H2], acci[H2];
+#pragma unroll
+    for (int c = 0; c < H2; ++c) accr[c] = acci[c] = 0;
+    bool touched = false;
+    int tile = -1;
+    for (;; ++k) {  // batches of the tile
+      const int slot = k % S;
+      mbar_wait(full + slot, (k / S) & 1);
+      const StageMeta mt = meta[slot];
+      if (mt.nb < 0) break;
+      tile = mt.tile;
+      const unsigned char* st = smem + slot * P::SB;
+      const double* ws = reinterpret_cast<const double*>(st);
+      const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
+      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
+      const int nb = (g.debug & 2) ? 0 : mt.nb;
+      int jb = 0;
+      int4 r = nb > 0 ? rs[0] : make_int4(0, 0, 0, 0);
+      while (jb < nb) {
+#define NFFTK_PIPE_NODE(H)                                                                   \
+    {                                                                                          \
+      const int ta = a - r.x, tb = b - r.y;                                                    \
+      const unsigned wp = (unsigned)r.w;                                                       \
+      const bool act = (unsigned)ta < (wp & 0xffu) && (unsigned)tb < ((wp >> 8) & 0xffu);      \
+      const double* w = ws + jb * PR;                                                          \
+      R cr = 0, ci = 0;                                                                        \
+      if (act) {                                                                               \
+        const R s = (R)(w[ta] * w[K + tb]);                                                    \
+        const C f = fv[jb];                                                                    \
+        cr = f.x * s;                                                                          \
+        ci = f.y * s;                                                                          \
+        touched = true;                                                                        \
+      }                                                                                        \
+      const double2* w2 = reinterpret_cast<const double2*>(w + 2 * K);                        \
+      _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                         \
+        const double2 v = w2[p];                                                               \
+        accr[H + 2 * p] = fma(cr, (R)v.x, accr[H + 2 * p]);                                    \
+        acci[H + 2 * p] = fma(ci, (R)v.x, acci[H + 2 * p]);                                    \
+        if (2 * p + 1 < K) {                                                                   \
+          accr[H + 2 * p + 1] = fma(cr, (R)v.y, accr[H + 2 * p + 1]);                          \
+          acci[H + 2 * p + 1] = fma(ci, (R)v.y, acci[H + 2 * p + 1]);                          \
+        }                                                                                      \
+      }                                                                                        \
+    }
+#define NFFTK_PIPE_CASE(H)                                   \
+    case H:                                                    \
+      if constexpr (H + K <= H2) {                             \
+        for (;;) {                                             \
+          NFFTK_PIPE_NODE(H)                                   \
+          if (++jb >= nb) break;                               \
+          r = rs[jb];                                          \
+          if (r.z != H) break;                                 \
+        }                                                      \
+      } else {                                                 \
+        if (++jb < nb) r = rs[jb];                             \
+      }                                                        \
+      break;
+        switch (r.z) {
+          NFFTK_PIPE_CASE(0) NFFTK_PIPE_CASE(1) NFFTK_PIPE_CASE(2) NFFTK_PIPE_CASE(3)
+          NFFTK_PIPE_CASE(4) NFFTK_PIPE_CASE(5) NFFTK_PIPE_CASE(6) NFFTK_PIPE_CASE(7)
+          NFFTK_PIPE_CASE(8)
+          default:
+            if (++jb < nb) r = rs[jb];
+            break;
+        }
+#undef NFFTK_PIPE_CASE
+#undef NFFTK_PIPE_NODE
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (threadIdx.x == 0) produce();
+      if (mt.last) {
+        ++k;
+        break;
+      }
+    }
+    if (tile < 0) break;  // end of work
+    // tile done: each thread stages and bulk-reduces its own row -- no CTA
+    // barrier; the row slot is reused only after this thread's previous
+    // reduction finished reading it
+    if (owner && touched && !(g.debug & 1)) {
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      C* dst = stage + (size_t)row * HS;
+#pragma unroll
+      for (int c = 0; c < H2; ++c) {
+        C v;
+        v.x = accr[c];
+        v.y = acci[c];
+        dst[c] = v;
+      }
+      if constexpr (HS > H2) {
+        C z;
+        z.x = 0;
+        z.y = 0;
+        dst[H2] = z;
+      }
+      fence_proxy_async_smem();
+      int tc[3];
+      tile_of<3>(g, tile, tc);
+      int64_t row0 = ((int64_t)(tc[0] * 8 + a) * g.np[1] + tc[1] * 8 + b) * g.np[2] + tc[2] * 8;
+      bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+      asm volatile("cp.async.bulk.commit_group;\n" ::);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+bool spread_pipe_ok(const Geom& g, int elem_bytes) {
+  (void)elem_bytes;
+  return g.d == 3 && g.mode == MODE_TENSOR && g.psi && g.rec && g.m >= 1 && g.m <= 6 &&
+         g.T[0] == 8 && g.T[1] == 8 && g.T[2] == 8 && !getenv("NFFTK_NO_PIPE");
+}
+
 size_t spread_rr_smem(const Geom& g, int elem_bytes) {
   const int K = 2 * g.m + 1;
   auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
@@ -825,6 +1098,28 @@ template <typename R, int D, int MM>
 static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const double* xs,
                       const int*, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if constexpr (D == 3 && MM > 0) {
+    if constexpr (MM <= 6) {
+      if (spread_pipe_ok(g, sizeof(cplx_t<R>))) {
+        using P = PipeCfg<R, MM>;
+        static_assert(P::NB > 0 && P::S >= 2, "pipe ring does not fit");
+        if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
+        auto kern = k_spread_pipe<R, MM>;
+        NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
+        static int sms = 0;
+        if (!sms) {
+          int dev = 0;
+          NFFTK_CUDA(cudaGetDevice(&dev));
+          NFFTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+        int per_sm = 0;
+        NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
+        int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
+        kern<<<grid, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs,
+                                               nsubs, g);
+        count_launch();
+        return;
+      }
+    }
     if (spread_rr_ok(g, sizeof(cplx_t<R>))) {
       const int threads = (g.H[0] * g.H[1] + 31) & ~31;
       size_t smem = spread_rr_smem(g, sizeof(cplx_t<R>));

@@ -47,21 +47,25 @@ void launch_check_range(const double* x, int64_t count, unsigned long long* firs
 
 // ---------------------------------------------------------------- binning
 // Sort key = tile-major cell index: tile (row-major over the tile grid) times
-// T^d plus the cell's row-major offset inside the tile.  Cells are the slots
-// floor(n x) mod n (kernels.py:47 wrapping, plan.py:229 cell definition).
+// T^d plus the cell's offset inside the tile, LAST dim most significant --
+// nodes of a tile come grouped by their last-dim stencil offset, which the
+// register-resident spread dispatches on once per run instead of per node.
+// Cells are the slots floor(n x) mod n (kernels.py:47 wrapping, plan.py:229
+// cell definition).
 __global__ void k_bin_keys(const double* __restrict__ x, int64_t M, Geom g,
                            uint32_t* __restrict__ keys, int* __restrict__ vals,
                            int* __restrict__ tile_count) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t tile = 0, local = 0;
+    uint32_t tile = 0, local = 0, lc[MAX_D];
     for (int dim = 0; dim < g.d; ++dim) {
       double y = __dmul_rn(x[i * g.d + dim], g.nd[dim]);
       int64_t s = floor_mod((int64_t)floor(y), g.n[dim]);
       int tcoord = (int)(s / g.T[dim]);
       tile = tile * g.ntile[dim] + tcoord;
-      local = local * g.T[dim] + (uint32_t)(s - (int64_t)tcoord * g.T[dim]);
+      lc[dim] = (uint32_t)(s - (int64_t)tcoord * g.T[dim]);
     }
+    for (int dim = g.d - 1; dim >= 0; --dim) local = local * g.T[dim] + lc[dim];
     uint32_t tvol = 1;
     for (int dim = 0; dim < g.d; ++dim) tvol *= g.T[dim];
     keys[i] = tile * tvol + local;
@@ -112,18 +116,51 @@ __global__ void k_sum_widths(const double* __restrict__ xs, int64_t M, Geom g,
 // PRE_PSI table (kernels.py:56-72), sorted node order, zero-filled past width.
 __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
                             double* __restrict__ psi) {
-  const int K = 2 * g.m + 1;
-  const int64_t total = M * g.d * K;
+  const int K = 2 * g.m + 1, pr = psi_row(g.d, K);
+  const int64_t total = M * pr;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
        q += (int64_t)gridDim.x * blockDim.x) {
-    int t = (int)(q % K);
-    int64_t r = q / K;
-    int dim = (int)(r % g.d);
-    int64_t i = r / g.d;
+    int64_t i = q / pr;
+    int r = (int)(q - i * pr);
+    int dim = r / K, t = r - dim * K;
+    if (dim >= g.d) {  // row padding
+      psi[q] = 0.0;
+      continue;
+    }
     double x = xs[dim * M + i];
     Stencil st = stencil(x, g.nd[dim], g.md);
     psi[q] = t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0;
   }
+}
+
+// Per-node stencil records in sorted order: halo-relative stencil starts
+// h[dim] = (cell slot - tile start) + m - (cell - lo) and widths, packed
+// {h0, h1, h2, W0 | W1 << 8 | W2 << 16 | fast << 24}.  The tile is the one
+// k_bin_keys assigned (same slot arithmetic), so the spread reads one 16-byte
+// record per node instead of recomputing stencils from coordinates.
+__global__ void k_build_recs(const double* __restrict__ xs, int64_t M, Geom g,
+                             int4* __restrict__ rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int h[3] = {0, 0, 0};
+    unsigned packed = 0;
+    bool fast = true;
+    for (int dim = 0; dim < g.d; ++dim) {
+      Stencil st = stencil(xs[dim * M + i], g.nd[dim], g.md);
+      int64_t slot = floor_mod(st.cell, g.n[dim]);
+      int tcoord = (int)(slot / g.T[dim]);
+      h[dim] = (int)(slot - (int64_t)tcoord * g.T[dim]) + g.m - (int)(st.cell - st.lo);
+      packed |= (unsigned)st.width << (8 * dim);
+      fast = fast && st.width == 2 * g.m;
+    }
+    packed |= (unsigned)fast << 24;
+    rec[i] = make_int4(h[0], h[1], h[2], (int)packed);
+  }
+}
+
+void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, cudaStream_t s) {
+  k_build_recs<<<blocks_for(M, 256), 256, 0, s>>>(xs, M, g, rec);
+  count_launch();
 }
 
 // Lexicographic cell order (plan.py:228-231): stable sort of (floor(n x)
@@ -213,7 +250,7 @@ unsigned long long sum_widths(const double* xs, int64_t M, const Geom& g, cudaSt
 }
 
 void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s) {
-  k_build_psi<<<blocks_for(M * g.d * (2 * g.m + 1), 256), 256, 0, s>>>(xs, M, g, psi);
+  k_build_psi<<<blocks_for(M * psi_row(g.d, 2 * g.m + 1), 256), 256, 0, s>>>(xs, M, g, psi);
   count_launch();
 }
 

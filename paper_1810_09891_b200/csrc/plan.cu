@@ -114,6 +114,7 @@ Plan::~Plan() {
   cudaFree(tile_count);
   cudaFree(subs);
   cudaFree(psi);
+  cudaFree(rec);
   cudaFree(lut);
   cudaFree(cols);
   if (!grid_external) cudaFree(grid);
@@ -383,6 +384,9 @@ static void nodes_to_device(Plan* p, cudaStream_t s) {
   bin_and_sort(p->x_dev, M, p->geom, p->maxsub, p->ntiles, p->perm, p->xs, p->tile_count,
                p->tile_start, &p->subs, &p->nsubs, s);
   p->width_sum = sum_widths(p->xs, M, p->geom, s);
+  if (!p->rec) NFFTK_CUDA(cudaMalloc(&p->rec, sizeof(int4) * M));
+  build_recs(p->xs, M, p->geom, p->rec, s);
+  p->geom.rec = p->rec;
 }
 
 static void invalidate_tables(Plan* p) {
@@ -547,7 +551,7 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   p->geom.mode = MODE_DIRECT;  // psi table itself is built from exact factors
   p->geom.psi = nullptr;
   if (mode == MODE_TENSOR) {
-    size_t count = (size_t)p->M * p->d * (2 * p->m + 1);
+    size_t count = (size_t)p->M * psi_row(p->d, 2 * p->m + 1);
     if (!p->psi) NFFTK_CUDA(cudaMalloc(&p->psi, sizeof(double) * count));
     build_psi(p->xs, p->M, p->geom, p->psi, s);
     p->geom.psi = p->psi;
@@ -599,7 +603,7 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
   { PhaseScope ps(p, PH_ZERO, s); NFFTK_CUDA(cudaMemsetAsync(p->gp, 0, p->gp_bytes, s)); }
-  if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * p->M));
+  if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * (p->M + 2)));  // +2: aligned bulk copies
   { PhaseScope ps(p, PH_PERMUTE, s); launch_permute(p->single, f, p->perm, p->M, p->f_sorted, s); }
   { PhaseScope ps(p, PH_SPREAD, s);
     launch_spread(p->single, p->gp, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }

@@ -53,6 +53,7 @@ struct Plan {
   int* tile_start = nullptr;
   int4* subs = nullptr;
   double* psi = nullptr;
+  int4* rec = nullptr;              // per-node stencil records, sorted order
   double* lut = nullptr;
   double* cols = nullptr;
   void* grid = nullptr;              // dense n-grid (cuFFT, deconvolution)
