@@ -946,14 +946,13 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       const unsigned wp = (unsigned)r.w;                                                       \
       const bool act = (unsigned)ta < (wp & 0xffu) && (unsigned)tb < ((wp >> 8) & 0xffu);      \
       const double* w = ws + jb * PR;                                                          \
-      R cr = 0, ci = 0;                                                                        \
-      if (act) {                                                                               \
-        const R s = (R)(w[ta] * w[K + tb]);                                                    \
-        const C f = fv[jb];                                                                    \
-        cr = f.x * s;                                                                          \
-        ci = f.y * s;                                                                          \
-        touched = true;                                                                        \
-      }                                                                                        \
+      /* branch-free: clamped loads, product zeroed off the stencil */                        \
+      const double s0 = w[min((unsigned)ta, (unsigned)(K - 1))] *                              \
+                        w[K + min((unsigned)tb, (unsigned)(K - 1))];                           \
+      const R s = act ? (R)s0 : (R)0;                                                          \
+      touched |= act;                                                                          \
+      const C f = fv[jb];                                                                      \
+      const R cr = f.x * s, ci = f.y * s;                                                      \
       const double2* w2 = reinterpret_cast<const double2*>(w + 2 * K);                        \
       _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                         \
         const double2 v = w2[p];                                                               \
@@ -1026,6 +1025,211 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     }
   }
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+// ------------------------------------- C'': pipelined register spread, d = 2
+// One warp per CTA, one 32-row halo per tile: lane l owns halo row a = l
+// (T0 = 32 - (2m+1)) and keeps its H1 = T1 + 2m + 1 cells in registers.  A
+// node is 2m+1 FMA pairs on the lanes inside its row window; batches arrive
+// on the same TMA/mbarrier ring as the d = 3 kernel (lane 0 produces, lag 1),
+// nodes come in runs of equal last-dim stencil start, and each lane
+// bulk-reduces its own row at the end of a tile.
+template <typename R, int MM, int T1>
+struct Pipe2Cfg {
+  static constexpr int K = 2 * MM + 1;
+  static constexpr int H0 = 32;
+  static constexpr int H1 = T1 + K;
+  static constexpr int ELEM = 2 * (int)sizeof(R);
+  static constexpr int HS = ELEM == 8 ? H1 + (H1 & 1) : H1;  // 16-byte rows
+  static constexpr int PR = 2 * K;                            // psi_row(2, K)
+  static constexpr int NB = 16;
+  static constexpr int S = 4;
+  static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
+  static constexpr size_t W_BYTES = al(sizeof(double) * NB * PR);
+  static constexpr size_t R_BYTES = al(16 * (size_t)NB);
+  static constexpr size_t SB = W_BYTES + R_BYTES + al((size_t)ELEM * (NB + 2));
+  static constexpr size_t CTL = S * SB;
+  static constexpr size_t ROWS_OFF = CTL + al(16 * (size_t)S + sizeof(StageMeta) * S + 32);
+  static constexpr size_t SMEM = ROWS_OFF + al((size_t)H0 * HS * ELEM);
+};
+
+template <typename R, int MM, int T1>
+__global__ void __launch_bounds__(32)
+k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
+               const double* __restrict__ psi, const int4* __restrict__ rec,
+               const int4* __restrict__ subs, int nsubs, Geom g) {
+  using C = cplx_t<R>;
+  using P = Pipe2Cfg<R, MM, T1>;
+  constexpr int K = P::K, H1 = P::H1, HS = P::HS, PR = P::PR, NB = P::NB, S = P::S;
+  constexpr int FA = 16 / (int)sizeof(C);
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
+  unsigned long long* empty = full + S;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + S);
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k
+  C* stage = reinterpret_cast<C*>(smem + P::ROWS_OFF);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    pst[0] = blockIdx.x;
+    pst[4] = 0;
+    if (blockIdx.x < nsubs) {
+      const int4 sp = subs[blockIdx.x];
+      pst[1] = sp.y;
+      pst[2] = sp.y + sp.z;
+      pst[3] = sp.x;
+    }
+  }
+  __syncwarp();
+  auto produce = [&]() {
+    const int pk = pst[4];
+    const int slot = pk % S;
+    if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
+    StageMeta* mt = meta + slot;
+    pst[4] = pk + 1;
+    if (pst[0] >= nsubs) {
+      mt->nb = -1;
+      mbar_arrive(full + slot);
+      return;
+    }
+    const int pbase = pst[1], pend = pst[2];
+    const int nb = min(NB, pend - pbase);
+    const int foff = pbase & (FA - 1);
+    const int fcnt = (nb + foff + FA - 1) & ~(FA - 1);
+    mt->tile = pst[3];
+    mt->nb = nb;
+    mt->last = pbase + nb >= pend;
+    mt->foff = foff;
+    unsigned char* st = smem + slot * P::SB;
+    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb,
+                   fb = (unsigned)sizeof(C) * fcnt;
+    mbar_expect_tx(full + slot, wb + rb + fb);
+    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
+    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (pbase + nb < pend) {
+      pst[1] = pbase + nb;
+    } else {
+      const int s = pst[0] + gridDim.x;
+      pst[0] = s;
+      if (s < nsubs) {
+        const int4 sp = subs[s];
+        pst[1] = sp.y;
+        pst[2] = sp.y + sp.z;
+        pst[3] = sp.x;
+      }
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < S - 1; ++i) produce();
+  __syncwarp();
+
+  const int a = lane;
+  int k = 0;
+  for (;;) {  // tiles of this CTA
+    R accr[H1], acci[H1];
+#pragma unroll
+    for (int c = 0; c < H1; ++c) accr[c] = acci[c] = 0;
+    int tile = -1;
+    for (;; ++k) {  // batches of the tile
+      const int slot = k % S;
+      mbar_wait(full + slot, (k / S) & 1);
+      const StageMeta mt = meta[slot];
+      if (mt.nb < 0) break;
+      tile = mt.tile;
+      const unsigned char* st = smem + slot * P::SB;
+      const double* ws = reinterpret_cast<const double*>(st);
+      const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
+      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
+      const int nb = (g.debug & 2) ? 0 : mt.nb;
+      int jb = 0;
+      int4 r = nb > 0 ? rs[0] : make_int4(0, 0, 0, 0);
+      while (jb < nb) {
+#define NFFTK_PIPE2_NODE(H)                                                                    \
+  {                                                                                            \
+    const int ta = a - r.x;                                                                    \
+    const bool act = (unsigned)ta < ((unsigned)r.w & 0xffu);                                   \
+    const double* w = ws + jb * PR;                                                            \
+    const double s0 = w[min((unsigned)ta, (unsigned)(K - 1))];                                 \
+    const R s = act ? (R)s0 : (R)0;                                                            \
+    const C f = fv[jb];                                                                        \
+    const R cr = f.x * s, ci = f.y * s;                                                        \
+    const double* w1 = w + K;                                                                  \
+    _Pragma("unroll") for (int t = 0; t < K; ++t) {                                            \
+      accr[H + t] = fma(cr, (R)w1[t], accr[H + t]);                                            \
+      acci[H + t] = fma(ci, (R)w1[t], acci[H + t]);                                            \
+    }                                                                                          \
+  }
+#define NFFTK_PIPE2_CASE(H)                                  \
+  case H:                                                    \
+    if constexpr (H + K <= H1) {                             \
+      for (;;) {                                             \
+        NFFTK_PIPE2_NODE(H)                                  \
+        if (++jb >= nb) break;                               \
+        r = rs[jb];                                          \
+        if (r.y != H) break;                                 \
+      }                                                      \
+    } else {                                                 \
+      if (++jb < nb) r = rs[jb];                             \
+    }                                                        \
+    break;
+        switch (r.y) {
+          NFFTK_PIPE2_CASE(0) NFFTK_PIPE2_CASE(1) NFFTK_PIPE2_CASE(2) NFFTK_PIPE2_CASE(3)
+          NFFTK_PIPE2_CASE(4) NFFTK_PIPE2_CASE(5) NFFTK_PIPE2_CASE(6) NFFTK_PIPE2_CASE(7)
+          NFFTK_PIPE2_CASE(8) NFFTK_PIPE2_CASE(9) NFFTK_PIPE2_CASE(10) NFFTK_PIPE2_CASE(11)
+          NFFTK_PIPE2_CASE(12) NFFTK_PIPE2_CASE(13) NFFTK_PIPE2_CASE(14) NFFTK_PIPE2_CASE(15)
+          NFFTK_PIPE2_CASE(16)
+          default:
+            if (++jb < nb) r = rs[jb];
+            break;
+        }
+#undef NFFTK_PIPE2_CASE
+#undef NFFTK_PIPE2_NODE
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty + slot);
+        produce();
+      }
+      __syncwarp();
+      if (mt.last) {
+        ++k;
+        break;
+      }
+    }
+    if (tile < 0) break;  // end of work
+    if (!(g.debug & 1)) {
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      C* dst = stage + (size_t)a * HS;
+#pragma unroll
+      for (int c = 0; c < H1; ++c) {
+        C v;
+        v.x = accr[c];
+        v.y = acci[c];
+        dst[c] = v;
+      }
+      if constexpr (HS > H1) {
+        C z;
+        z.x = 0;
+        z.y = 0;
+        dst[H1] = z;
+      }
+      fence_proxy_async_smem();
+      const int t0 = tile / g.ntile[1], t1 = tile - t0 * g.ntile[1];
+      int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
+      bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+      asm volatile("cp.async.bulk.commit_group;\n" ::);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+bool spread2_pipe_ok(const Geom& g) {
+  return g.d == 2 && g.mode == MODE_TENSOR && g.psi && g.rec && g.m >= 1 && g.m <= 8 &&
+         g.H[0] == 32 && g.T[1] == 8 && !getenv("NFFTK_NO_PIPE");
 }
 
 bool spread_pipe_ok(const Geom& g, int elem_bytes) {
@@ -1136,6 +1340,26 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
       NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
       int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
       kern<<<grid, threads, smem, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, xs, subs, nsubs, g);
+      count_launch();
+      return;
+    }
+  }
+  if constexpr (D == 2 && MM > 0) {
+    if (spread2_pipe_ok(g)) {
+      using P = Pipe2Cfg<R, MM, 8>;
+      if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
+      auto kern = k_spread2_pipe<R, MM, 8>;
+      NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
+      static int sms2 = 0;
+      if (!sms2) {
+        int dev = 0;
+        NFFTK_CUDA(cudaGetDevice(&dev));
+        NFFTK_CUDA(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev));
+      }
+      int per_sm = 0;
+      NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, P::SMEM));
+      int grid = std::max(1, std::min(nsubs, sms2 * std::max(1, per_sm)));
+      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs, nsubs, g);
       count_launch();
       return;
     }

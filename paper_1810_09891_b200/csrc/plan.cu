@@ -179,9 +179,23 @@ static void choose_tiles(Plan* p) {
     return true;
   };
   while (T > 2 && !fits(T)) T /= 2;
+  int Td[MAX_D];
+  for (int i = 0; i < p->d; ++i) Td[i] = std::min(T, p->n[i]);
+  // d = 2 register-resident spread: 32 halo rows (one warp) x (8 + 2m + 1)
+  if (p->d == 2 && !force && p->m <= 8 && !getenv("NFFTK_NO_PIPE")) {
+    const int t0 = 32 - (2 * p->m + 1), t1 = 8;
+    auto fits1 = [&](int i, int ti) {
+      int nt = (p->n[i] + ti - 1) / ti;
+      return ti <= p->n[i] && nt * ti + p->m + 2 <= 2 * p->n[i];
+    };
+    if (fits1(0, t0) && fits1(1, t1)) {
+      Td[0] = t0;
+      Td[1] = t1;
+    }
+  }
   p->ntiles = 1;
   for (int i = 0; i < p->d; ++i) {
-    g.T[i] = std::min(T, p->n[i]);
+    g.T[i] = Td[i];
     g.H[i] = g.T[i] + 2 * p->m + 1;
     g.ntile[i] = (p->n[i] + g.T[i] - 1) / g.T[i];
     p->ntiles *= g.ntile[i];
