@@ -241,6 +241,93 @@ struct InterpTeam {
 // one is processed.  A team of TEAM lanes reduces one node: lanes split the
 // leading stencil dims and run along the contiguous last dim with the factors
 // in registers; a team shuffle reduction forms f_j.
+// One node of the interpolation, this lane's share (lane tl of a TEAM):
+// q = {h_0..h_{D-1}, W_0..W_{D-1}, fast}, w = the node's factor row.
+template <typename R, int D, int MM, int TEAM>
+__device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, int HS, int H1, int K,
+                                            const int* q, const double* w, int tl, R& are, R& aim) {
+  using C = cplx_t<R>;
+  if (MM > 0 && q[2 * D]) {
+    constexpr int WF = 2 * (MM > 0 ? MM : 1);
+    if constexpr (D == 1) {
+      for (int t0 = tl; t0 < WF; t0 += TEAM) {
+        C v = halo[q[0] + t0];
+        R ww = (R)w[t0];
+        are = fma(ww, v.x, are);
+        aim = fma(ww, v.y, aim);
+      }
+    } else if constexpr (D == 2) {
+      // lanes own whole stencil rows: a TEAM of consecutive halo rows hits
+      // distinct shared-memory banks (odd row stride)
+      R w1r[WF];
+#pragma unroll
+      for (int t = 0; t < WF; ++t) w1r[t] = (R)w[K + t];
+      for (int t0 = tl; t0 < WF; t0 += TEAM) {
+        const C* row = halo + (q[0] + t0) * HS + q[1];
+        R sre = 0, sim = 0;
+#pragma unroll
+        for (int t = 0; t < WF; ++t) {
+          C v = row[t];
+          sre = fma(w1r[t], v.x, sre);
+          sim = fma(w1r[t], v.y, sim);
+        }
+        R w0 = (R)w[t0];
+        are = fma(w0, sre, are);
+        aim = fma(w0, sim, aim);
+      }
+    } else {
+      R w2r[WF];
+#pragma unroll
+      for (int t = 0; t < WF; ++t) w2r[t] = (R)w[2 * K + t];
+      const C* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
+#pragma unroll 2
+      for (int p = tl; p < WF * WF; p += TEAM) {
+        int t0 = p / WF, t1 = p - t0 * WF;
+        const C* row = corner + (t0 * H1 + t1) * HS;
+        R sre = 0, sim = 0;
+#pragma unroll
+        for (int t = 0; t < WF; ++t) {
+          C v = row[t];
+          sre = fma(w2r[t], v.x, sre);
+          sim = fma(w2r[t], v.y, sim);
+        }
+        R w01 = (R)(w[t0] * w[K + t1]);
+        are = fma(w01, sre, are);
+        aim = fma(w01, sim, aim);
+      }
+    }
+  } else {
+    // generic widths (2m or 2m+1 per dim), runtime loops
+    if constexpr (D == 1) {
+      for (int t0 = tl; t0 < q[1]; t0 += TEAM) {
+        C v = halo[q[0] + t0];
+        R ww = (R)w[t0];
+        are = fma(ww, v.x, are);
+        aim = fma(ww, v.y, aim);
+      }
+    } else {
+      const int WL = q[2 * D - 1];
+      const int P = D == 2 ? q[D] : q[D] * q[D + 1];
+      const int W1 = D == 3 ? q[D + 1] : 1;
+      const double* wl = w + (D - 1) * K;
+      for (int p = tl; p < P; p += TEAM) {
+        int t0 = p / W1, t1 = p - t0 * W1;
+        const C* row = D == 2 ? halo + (q[0] + t0) * HS + q[1]
+                              : halo + ((q[0] + t0) * H1 + q[1] + t1) * HS + q[D - 1];
+        R sre = 0, sim = 0;
+        for (int t = 0; t < WL; ++t) {
+          C v = row[t];
+          sre = fma((R)wl[t], v.x, sre);
+          sim = fma((R)wl[t], v.y, sim);
+        }
+        R wr = (R)(D == 2 ? w[t0] : w[t0] * w[K + t1]);
+        are = fma(wr, sre, are);
+        aim = fma(wr, sim, aim);
+      }
+    }
+  }
+}
+
 constexpr int INTERP_NB = 32;
 
 template <typename R, int D, int MM>
@@ -307,86 +394,7 @@ k_interp(const __grid_constant__ CUtensorMap tmap, const cplx_t<R>* __restrict__
       const int* q = cur.hw + (active ? jb : j0) * (2 * D + 2);
       const double* w = cur.w + (active ? jb : j0) * psi_row(D, K);
       R are = 0, aim = 0;
-      if (active) {
-        if (MM > 0 && q[2 * D]) {
-          constexpr int WF = 2 * (MM > 0 ? MM : 1);
-          if constexpr (D == 1) {
-            for (int t0 = tl; t0 < WF; t0 += TEAM) {
-              C v = halo[q[0] + t0];
-              R ww = (R)w[t0];
-              are = fma(ww, v.x, are);
-              aim = fma(ww, v.y, aim);
-            }
-          } else if constexpr (D == 2) {
-            constexpr int SEG = WF / 2;
-            for (int p = tl; p < 2 * WF; p += TEAM) {
-              int t0 = p >> 1, seg = p & 1;
-              const C* row = halo + (q[0] + t0) * HS + q[1] + seg * SEG;
-              const double* w1 = w + K + seg * SEG;
-              R sre = 0, sim = 0;
-#pragma unroll
-              for (int t = 0; t < SEG; ++t) {
-                C v = row[t];
-                R ww = (R)w1[t];
-                sre = fma(ww, v.x, sre);
-                sim = fma(ww, v.y, sim);
-              }
-              R w0 = (R)w[t0];
-              are = fma(w0, sre, are);
-              aim = fma(w0, sim, aim);
-            }
-          } else {
-            R w2r[WF];
-#pragma unroll
-            for (int t = 0; t < WF; ++t) w2r[t] = (R)w[2 * K + t];
-            const C* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
-#pragma unroll 2
-            for (int p = tl; p < WF * WF; p += TEAM) {
-              int t0 = p / WF, t1 = p - t0 * WF;
-              const C* row = corner + (t0 * H1 + t1) * HS;
-              R sre = 0, sim = 0;
-#pragma unroll
-              for (int t = 0; t < WF; ++t) {
-                C v = row[t];
-                sre = fma(w2r[t], v.x, sre);
-                sim = fma(w2r[t], v.y, sim);
-              }
-              R w01 = (R)(w[t0] * w[K + t1]);
-              are = fma(w01, sre, are);
-              aim = fma(w01, sim, aim);
-            }
-          }
-        } else {
-          // generic widths (2m or 2m+1 per dim), runtime loops
-          if constexpr (D == 1) {
-            for (int t0 = tl; t0 < q[1]; t0 += TEAM) {
-              C v = halo[q[0] + t0];
-              R ww = (R)w[t0];
-              are = fma(ww, v.x, are);
-              aim = fma(ww, v.y, aim);
-            }
-          } else {
-            const int WL = q[2 * D - 1];
-            const int P = D == 2 ? q[D] : q[D] * q[D + 1];
-            const int W1 = D == 3 ? q[D + 1] : 1;
-            const double* wl = w + (D - 1) * K;
-            for (int p = tl; p < P; p += TEAM) {
-              int t0 = p / W1, t1 = p - t0 * W1;
-              const C* row = D == 2 ? halo + (q[0] + t0) * HS + q[1]
-                                    : halo + ((q[0] + t0) * H1 + q[1] + t1) * HS + q[D - 1];
-              R sre = 0, sim = 0;
-              for (int t = 0; t < WL; ++t) {
-                C v = row[t];
-                sre = fma((R)wl[t], v.x, sre);
-                sim = fma((R)wl[t], v.y, sim);
-              }
-              R wr = (R)(D == 2 ? w[t0] : w[t0] * w[K + t1]);
-              are = fma(wr, sre, are);
-              aim = fma(wr, sim, aim);
-            }
-          }
-        }
-      }
+      if (active) interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, tl, are, aim);
 #pragma unroll
       for (int o = TEAM / 2; o; o >>= 1) {
         are += __shfl_xor_sync(0xffffffffu, are, o);
@@ -400,6 +408,208 @@ k_interp(const __grid_constant__ CUtensorMap tmap, const cplx_t<R>* __restrict__
       }
     }
   }
+}
+
+// ---------------------------------------- B': pipelined interpolation
+// PRE_PSI (tensor) mode, d = 2 / 3.  Persistent CTAs walk their
+// subproblems; the halo of each comes by one TMA tensor copy (double
+// buffered when two halos fit, so the next halo loads under the current
+// tile), node batches (PRE_PSI rows, stencil records, output indices) by TMA
+// bulk copies on an mbarrier ring refilled by thread 0 -- no coordinate
+// loads, no stencil arithmetic, one CTA barrier per tile instead of two per
+// batch.  Per node the TEAM-lane gather of interp_node.
+struct StageMetaI {
+  int nb;    // nodes (< 0: end of work)
+  int last;  // last batch of its subproblem
+  int poff;  // output-index offset inside the stage (alignment of the bulk copy)
+  int pad;
+};
+
+template <typename R, int D, int MM>
+struct IPipeCfg {
+  static constexpr int K = 2 * MM + 1;
+  static constexpr int H0 = D == 3 ? 8 + K : 32;
+  static constexpr int H1 = D == 3 ? 8 + K : 1;
+  static constexpr int HL = 8 + K;                      // last-dim halo edge
+  static constexpr int ELEM = 2 * (int)sizeof(R);
+  static constexpr int HS = ELEM == 8 ? HL + (HL & 1) : HL;
+  static constexpr int ROWS = H0 * H1;
+  static constexpr int THREADS = D == 3 ? 512 : 256;
+  static constexpr int TEAM = InterpTeam<D, MM>::value;
+  static constexpr int NPASS = (32 / TEAM) * (THREADS / 32);  // nodes per CTA pass
+  static constexpr int NB = NPASS < 16 ? 16 : (NPASS > 64 ? 64 : NPASS);
+  static constexpr int PR = (D * K + 1) & ~1;
+  static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
+  static constexpr size_t W_BYTES = al(sizeof(double) * NB * PR);
+  static constexpr size_t R_BYTES = al(16 * (size_t)NB);
+  static constexpr size_t SB = W_BYTES + R_BYTES + al(4 * (size_t)(NB + 4));
+  static constexpr size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
+  static constexpr size_t HALO = al128((size_t)ROWS * HS * ELEM);  // TMA tensor destinations: 128 B
+  static constexpr int S = 4;
+  static constexpr size_t CTL = S * SB;
+  static constexpr size_t CTL_BYTES = al(16 * (size_t)S + sizeof(StageMetaI) * S + 32 + 16);
+  static constexpr size_t HALO_OFF = al128(CTL + CTL_BYTES);
+  static constexpr int NH = HALO_OFF + 2 * HALO <= 224 * 1024 ? 2 : 1;
+  static constexpr size_t SMEM = HALO_OFF + NH * HALO;
+};
+
+template <typename R, int D, int MM>
+__global__ void __launch_bounds__(IPipeCfg<R, D, MM>::THREADS, 1)
+k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ fout,
+              const double* __restrict__ psi, const int4* __restrict__ rec,
+              const int* __restrict__ perm, const int4* __restrict__ subs, int nsubs, Geom g) {
+  using C = cplx_t<R>;
+  using P = IPipeCfg<R, D, MM>;
+  constexpr int K = P::K, HS = P::HS, H1 = P::H1, PR = P::PR, NB = P::NB, S = P::S, NH = P::NH;
+  constexpr int TEAM = P::TEAM, NPW = 32 / TEAM, NW = P::THREADS / 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
+  unsigned long long* empty = full + S;
+  unsigned long long* hbar = empty + S;  // NH halo barriers
+  StageMetaI* meta = reinterpret_cast<StageMetaI*>(hbar + 2);
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, k
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tl = lane % TEAM, sub = lane / TEAM;
+  const unsigned halo_tx = (unsigned)(P::ROWS * HS * sizeof(C));
+  auto issue_halo = [&](int s, int buf) {
+    int tc[D];
+    tile_of<D>(g, subs[s].x, tc);
+    int c[3];
+    const int scale = sizeof(C) / 8;
+#pragma unroll
+    for (int i = 0; i < D; ++i) c[D - 1 - i] = tc[i] * g.T[i];
+    c[0] *= scale;
+    mbar_expect_tx(hbar + buf, halo_tx);
+    tma_load_box<D>(smem + P::HALO_OFF + buf * P::HALO, &tmap, c, hbar + buf);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NW);
+    }
+    for (int i = 0; i < NH; ++i) mbar_init(hbar + i, 1);
+    pst[0] = blockIdx.x;
+    pst[3] = 0;
+    if (blockIdx.x < nsubs) {
+      const int4 sp = subs[blockIdx.x];
+      pst[1] = sp.y;
+      pst[2] = sp.y + sp.z;
+    }
+  }
+  __syncthreads();
+  auto produce = [&]() {
+    const int pk = pst[3];
+    const int slot = pk % S;
+    if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
+    StageMetaI* mt = meta + slot;
+    pst[3] = pk + 1;
+    if (pst[0] >= nsubs) {
+      mt->nb = -1;
+      mbar_arrive(full + slot);
+      return;
+    }
+    const int pbase = pst[1], pend = pst[2];
+    const int nb = min(NB, pend - pbase);
+    const int poff = pbase & 3;
+    const int pcnt = (nb + poff + 3) & ~3;
+    mt->nb = nb;
+    mt->last = pbase + nb >= pend;
+    mt->poff = poff;
+    unsigned char* st = smem + slot * P::SB;
+    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb, pb = 4u * pcnt;
+    mbar_expect_tx(full + slot, wb + rb + pb);
+    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
+    bulk_g2s(st + P::W_BYTES + P::R_BYTES, perm + (pbase - poff), pb, full + slot);
+    if (pbase + nb < pend) {
+      pst[1] = pbase + nb;
+    } else {
+      const int s = pst[0] + gridDim.x;
+      pst[0] = s;
+      if (s < nsubs) {
+        const int4 sp = subs[s];
+        pst[1] = sp.y;
+        pst[2] = sp.y + sp.z;
+      }
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S - 1; ++i) produce();
+    if (NH == 2 && (int)blockIdx.x < nsubs) issue_halo(blockIdx.x, 0);
+  }
+  int k = 0;
+  int it = 0;
+  for (int s = blockIdx.x; s < nsubs; s += gridDim.x, ++it) {
+    const int buf = NH == 2 ? (it & 1) : 0;
+    __syncthreads();  // every warp is done with the halo buffer about to be refilled
+    if (threadIdx.x == 0) {
+      if constexpr (NH == 1) {
+        issue_halo(s, 0);
+      } else {
+        if (s + (int)gridDim.x < nsubs) issue_halo(s + gridDim.x, buf ^ 1);
+      }
+    }
+    mbar_wait(hbar + buf, (NH == 2 ? (it >> 1) : it) & 1);
+    const C* halo = reinterpret_cast<const C*>(smem + P::HALO_OFF + buf * P::HALO);
+    for (;; ++k) {  // batches of the subproblem
+      const int slot = k % S;
+      mbar_wait(full + slot, (k / S) & 1);
+      const StageMetaI mt = meta[slot];
+      const unsigned char* st = smem + slot * P::SB;
+      const double* ws = reinterpret_cast<const double*>(st);
+      const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
+      const int* pv = reinterpret_cast<const int*>(st + P::W_BYTES + P::R_BYTES) + mt.poff;
+      for (int j0 = warp * NPW; j0 < mt.nb; j0 += NW * NPW) {
+        const int jb = j0 + sub;
+        const bool active = jb < mt.nb;
+        const int jj = active ? jb : j0;
+        const int4 r = rs[jj];
+        const unsigned wp = (unsigned)r.w;
+        int q[8];
+        q[0] = r.x;
+        q[1] = r.y;
+        if constexpr (D == 3) {
+          q[2] = r.z;
+          q[3] = wp & 0xff;
+          q[4] = (wp >> 8) & 0xff;
+          q[5] = (wp >> 16) & 0xff;
+          q[6] = (wp >> 24) & 1;
+        } else {
+          q[2] = wp & 0xff;
+          q[3] = (wp >> 8) & 0xff;
+          q[4] = (wp >> 24) & 1;
+        }
+        R are = 0, aim = 0;
+        if (active) interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, ws + jj * PR, tl, are, aim);
+#pragma unroll
+        for (int o = TEAM / 2; o; o >>= 1) {
+          are += __shfl_xor_sync(0xffffffffu, are, o);
+          aim += __shfl_xor_sync(0xffffffffu, aim, o);
+        }
+        if (tl == 0 && active) {
+          C v;
+          v.x = are;
+          v.y = aim;
+          fout[pv[jb]] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (threadIdx.x == 0) produce();
+      if (mt.last) {
+        ++k;
+        break;
+      }
+    }
+  }
+}
+
+bool interp_pipe_ok(const Geom& g) {
+  if (!(g.mode == MODE_TENSOR && g.psi && g.rec && g.m >= 1 && g.m <= 8 && !getenv("NFFTK_NO_PIPE")))
+    return false;
+  if (g.d == 3) return g.T[0] == 8 && g.T[1] == 8 && g.T[2] == 8;
+  if (g.d == 2) return g.H[0] == 32 && g.T[1] == 8;
+  return false;
 }
 
 // Sorted copy of the samples for the spread: fs[i] = f[perm[i]].
@@ -1277,6 +1487,26 @@ int spread_threads(const Geom& g) {
 template <typename R, int D, int MM>
 static void interp_go(const CUtensorMap* tm, const void* gp, void* f, void*, const double* xs,
                       const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+  if constexpr (D >= 2 && MM > 0 && IPipeCfg<R, D, MM>::SMEM <= 224 * 1024) {
+    if (interp_pipe_ok(g)) {
+      using P = IPipeCfg<R, D, MM>;
+      if (g.HS != P::HS) fail(EK_CUDA, "pipe interp: halo row stride mismatch");
+      auto kern = k_interp_pipe<R, D, MM>;
+      NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        NFFTK_CUDA(cudaGetDevice(&dev));
+        NFFTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      int per_sm = 0;
+      NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
+      int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
+      kern<<<grid, P::THREADS, P::SMEM, s>>>(*tm, (cplx_t<R>*)f, g.psi, g.rec, perm, subs, nsubs, g);
+      count_launch();
+      return;
+    }
+  }
   const int threads = g.nt_interp;
   size_t smem = interp_smem(g, sizeof(cplx_t<R>), threads);
   auto kern = k_interp<R, D, MM>;

@@ -390,7 +390,7 @@ static void shape_check_x(const Plan* p, int64_t len) {
 static void nodes_to_device(Plan* p, cudaStream_t s) {
   const int64_t M = p->M;
   if (!p->xs) NFFTK_CUDA(cudaMalloc(&p->xs, sizeof(double) * M * p->d));
-  if (!p->perm) NFFTK_CUDA(cudaMalloc(&p->perm, sizeof(int) * M));
+  if (!p->perm) NFFTK_CUDA(cudaMalloc(&p->perm, sizeof(int) * (M + 4)));  // +4: aligned bulk copies
   if (!p->tile_count) {
     NFFTK_CUDA(cudaMalloc(&p->tile_count, sizeof(int) * (p->ntiles + 1) * 2));
     p->tile_start = p->tile_count + p->ntiles + 1;
