@@ -118,6 +118,8 @@ struct Geom {
   double lut_step[MAX_D];
   const double* psi;      // M * psi_row(d, 2m+1) in sorted order (MODE_TENSOR)
   const int4* rec;        // M per-node stencil records, sorted order
+  int psi_pad;            // PRE_PSI rows halo-indexed (pipelined kernels) vs stencil-indexed
+  int pr;                 // PRE_PSI row stride (doubles)
   int64_t M;
   int nt_interp;          // threads per interp CTA
   int np[MAX_D];          // ghost-padded grid (periodic images, halo = one box)
@@ -191,6 +193,15 @@ __device__ __forceinline__ double dim_factor(const Geom& g, int dim, double x, i
 // so every node row (and, for d = 3, the last-dim vector) is 16-byte aligned
 // for bulk copies and 128-bit shared loads.
 __host__ __device__ inline int psi_row(int d, int K) { return (d * K + 1) & ~1; }
+
+// Halo-indexed PRE_PSI row (pipelined kernels): every leading dim i as a row
+// of the tile halo's H_i cells (zero off the stencil, so a halo row reads its
+// factor without a stencil test), then the 2m+1 last-dim factors; even count.
+__host__ __device__ inline int psi_row_halo(int d, const int* H, int K) {
+  int s = K;
+  for (int i = 0; i + 1 < d; ++i) s += H[i];
+  return (s + 1) & ~1;
+}
 
 template <typename R> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };

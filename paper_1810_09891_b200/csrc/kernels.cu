@@ -116,21 +116,45 @@ __global__ void k_sum_widths(const double* __restrict__ xs, int64_t M, Geom g,
 // PRE_PSI table (kernels.py:56-72), sorted node order, zero-filled past width.
 __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
                             double* __restrict__ psi) {
-  const int K = 2 * g.m + 1, pr = psi_row(g.d, K);
+  const int K = 2 * g.m + 1, pr = g.pr;
   const int64_t total = M * pr;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
        q += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = q / pr;
     int r = (int)(q - i * pr);
-    int dim = r / K, t = r - dim * K;
-    if (dim >= g.d) {  // row padding
+    int dim = 0, t = r;
+    if (g.psi_pad) {
+      // halo-indexed leading dims, then the last dim's 2m+1 factors
+      while (dim + 1 < g.d && t >= g.H[dim]) t -= g.H[dim++];
+      if (dim + 1 == g.d && t >= K) dim = g.d;  // row padding
+    } else {
+      dim = r / K;
+      t = r - dim * K;
+    }
+    if (dim >= g.d) {
       psi[q] = 0.0;
       continue;
     }
     double x = xs[dim * M + i];
     Stencil st = stencil(x, g.nd[dim], g.md);
+    if (g.psi_pad && dim + 1 < g.d) {
+      // halo cell t -> stencil offset t - h (h as in k_build_recs)
+      int64_t slot = floor_mod(st.cell, g.n[dim]);
+      int tcoord = (int)(slot / g.T[dim]);
+      int h = (int)(slot - (int64_t)tcoord * g.T[dim]) + g.m - (int)(st.cell - st.lo);
+      t -= h;
+      if (t < 0) {
+        psi[q] = 0.0;
+        continue;
+      }
+    }
     psi[q] = t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0;
   }
+}
+
+void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s) {
+  k_build_psi<<<blocks_for(M * g.pr, 256), 256, 0, s>>>(xs, M, g, psi);
+  count_launch();
 }
 
 // Per-node stencil records in sorted order: halo-relative stencil starts
@@ -249,10 +273,6 @@ unsigned long long sum_widths(const double* xs, int64_t M, const Geom& g, cudaSt
   return total;
 }
 
-void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s) {
-  k_build_psi<<<blocks_for(M * psi_row(g.d, 2 * g.m + 1), 256), 256, 0, s>>>(xs, M, g, psi);
-  count_launch();
-}
 
 void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaStream_t s) {
   unsigned long long *keys = nullptr;

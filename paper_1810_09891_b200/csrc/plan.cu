@@ -564,8 +564,18 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   }
   p->geom.mode = MODE_DIRECT;  // psi table itself is built from exact factors
   p->geom.psi = nullptr;
+  p->geom.psi_pad = 0;
+  p->geom.pr = psi_row(p->d, 2 * p->m + 1);
   if (mode == MODE_TENSOR) {
-    size_t count = (size_t)p->M * psi_row(p->d, 2 * p->m + 1);
+    p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? 1 : 0;
+    p->geom.pr = p->geom.psi_pad ? psi_row_halo(p->d, p->geom.H, 2 * p->m + 1)
+                                 : psi_row(p->d, 2 * p->m + 1);
+    size_t count = (size_t)p->M * p->geom.pr;
+    if (p->psi && count != p->psi_count) {
+      cudaFree(p->psi);
+      p->psi = nullptr;
+    }
+    p->psi_count = count;
     if (!p->psi) NFFTK_CUDA(cudaMalloc(&p->psi, sizeof(double) * count));
     build_psi(p->xs, p->M, p->geom, p->psi, s);
     p->geom.psi = p->psi;

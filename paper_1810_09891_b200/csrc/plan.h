@@ -53,6 +53,7 @@ struct Plan {
   int* tile_start = nullptr;
   int4* subs = nullptr;
   double* psi = nullptr;
+  size_t psi_count = 0;
   int4* rec = nullptr;              // per-node stencil records, sorted order
   double* lut = nullptr;
   double* cols = nullptr;
