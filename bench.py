@@ -281,7 +281,8 @@ def main():
     # ---- roofline of the dominant gridding kernel
     peaks = measured_peaks()
     fp64, fp32 = ctypes_fma_peaks(_lib)
-    roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32)
+    roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32,
+                    tuple(plan.tile), args.psi)
 
     if rank != 0:
         if world > 1:
@@ -416,15 +417,26 @@ def ncu_traffic(config, kernel):
     return best
 
 
-def roofline(w, phases, steps, s, peaks, fma_tflops):
+def kernel_names(w, tile, psi):
+    """Names of the interp / spread kernels the library launches for this
+    workload (gridding.cu launchers): the pipelined register kernels in
+    PRE_PSI mode on their tile geometries, the batch kernels otherwise."""
+    tensor = psi in (None, "flags", "tensor")
+    k = 2 * w.m + 1
+    if tensor and w.d == 3 and w.m <= 6 and tuple(tile) == (8, 8, 8):
+        return {"interp": "k_interp_pipe", "spread": "k_spread_pipe"}
+    if tensor and w.d == 2 and w.m <= 8 and tuple(tile) == (32 - k, 8):
+        return {"interp": "k_interp_pipe", "spread": "k_spread2_pipe"}
+    rr = w.d == 3 and tuple(tile) == (8, 8, 8) and w.m <= 6
+    return {"interp": "k_interp", "spread": "k_spread_rr" if rr else "k_spread"}
+
+
+def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None):
     """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
     M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
     (4 w^d M flops with w = 2m).  Times are CUDA-event durations of the kernel
     launches inside the timed region (library phase events on the launch stream)."""
-    kernels = {
-        "interp": "k_interp",
-        "spread": "k_spread_rr" if (w.d == 3 and w.m <= 8 and min(w.n) >= 8) else "k_spread",
-    }
+    kernels = kernel_names(w, tile, psi)
     out = {}
     for ph, kname in kernels.items():
         ms, calls = phases.get(ph, (0.0, 0))
