@@ -1,0 +1,101 @@
+"""Parity of the pipelined register kernels (k_interp_pipe, k_spread_pipe,
+k_spread2_pipe) against the CPU oracle on their own tile geometries:
+d=3 with 8^3 tiles (forced with NFFTK_TILE on small grids), d=2 with 32-row
+halos, every cutoff they are instantiated for, complex128 and complex64.
+
+Edge cases the ring and the halo-indexed PRE_PSI rows must survive: grid-
+aligned nodes (stencil width 2m+1), nodes at -1/2 and just below +1/2 (halo
+wrap), batch counts around the ring's batch size, one dense cell (several
+subproblems of one tile), and a single node.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1810_09891_b200 as nf
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"double": 1e-12, "single": 1e-5}
+
+
+def e2(ref, got):
+    ref = np.asarray(ref).astype(np.complex128).ravel()
+    got = np.asarray(got).astype(np.complex128).ravel()
+    return float(np.linalg.norm(ref - got) / np.linalg.norm(ref))
+
+
+def nodes(d, n, M, seed, kind="uniform"):
+    rng = np.random.default_rng(seed)
+    if kind == "dense":  # everything in one cell of one tile
+        return (rng.random((M, d)) * 0.9 / n[0] + 0.1 / n[0]).astype(np.float64)
+    x = rng.random((M, d)) - 0.5
+    if kind == "edges":
+        k = max(1, M // 8)
+        x[:k] = rng.integers(-n[0] // 2, n[0] // 2, size=(k, d)) / np.array(n)  # aligned
+        x[k:2 * k, 0] = -0.5
+        x[2 * k:3 * k, -1] = np.nextafter(0.5, 0.0)
+    return x
+
+
+def plan(N, n, m, x, precision, monkeypatch, tile=None):
+    if tile:
+        monkeypatch.setenv("NFFTK_TILE", str(tile))
+    else:
+        monkeypatch.delenv("NFFTK_TILE", raising=False)
+    p = nf.Plan(N, x.shape[0], n=n, m=m, precision=precision)
+    p.x = x
+    p.precompute()
+    return p
+
+
+def check(p, N, n, m, x, oracle, precision):
+    rng = np.random.default_rng(7)
+    fh = rng.standard_normal(int(np.prod(N))) + 1j * rng.standard_normal(int(np.prod(N)))
+    fs = rng.standard_normal(x.shape[0]) + 1j * rng.standard_normal(x.shape[0])
+    assert p.mode == nf.MODE_TENSOR
+    assert e2(oracle.trafo(N, n, m, x, fh), p.trafo(fh)) < TOL[precision]
+    assert e2(oracle.adjoint(N, n, m, x, fs), p.adjoint(fs)) < TOL[precision]
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6])
+def test_pipe_d3_every_cutoff(m, precision, oracle, monkeypatch):
+    N, n = (8, 8, 8), (16, 16, 16)
+    x = nodes(3, n, 3000, seed=m, kind="edges")
+    p = plan(N, n, m, x, precision, monkeypatch, tile=8)
+    assert p.tile == (8, 8, 8)
+    check(p, N, n, m, x, oracle, precision)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("m", [1, 2, 4, 6, 8])
+def test_pipe_d2_every_cutoff(m, precision, oracle, monkeypatch):
+    N, n = (16, 16), (32, 32)
+    x = nodes(2, n, 3000, seed=10 + m, kind="edges")
+    p = plan(N, n, m, x, precision, monkeypatch)
+    assert p.tile == (32 - (2 * m + 1), 8)
+    check(p, N, n, m, x, oracle, precision)
+
+
+@pytest.mark.parametrize("M", [1, 15, 16, 17, 31, 32, 33, 64, 65])
+def test_pipe_batch_boundaries(M, oracle, monkeypatch):
+    N, n, m = (8, 8, 8), (16, 16, 16), 3
+    x = nodes(3, n, M, seed=M)
+    p = plan(N, n, m, x, "double", monkeypatch, tile=8)
+    check(p, N, n, m, x, oracle, "double")
+    N2, n2 = (16, 16), (32, 32)
+    x2 = nodes(2, n2, M, seed=100 + M)
+    p2 = plan(N2, n2, m, x2, "double", monkeypatch)
+    assert p2.tile == (32 - (2 * m + 1), 8)
+    check(p2, N2, n2, m, x2, oracle, "double")
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_pipe_dense_cell_many_subproblems(d, oracle, monkeypatch):
+    """5000 nodes in one cell: one tile split into several <= 1024-node
+    subproblems, each flushing its own halo."""
+    N, n, m = ((8, 8, 8), (16, 16, 16), 4) if d == 3 else ((16, 16), (32, 32), 6)
+    x = nodes(d, n, 5000, seed=3, kind="dense")
+    p = plan(N, n, m, x, "double", monkeypatch, tile=8 if d == 3 else None)
+    check(p, N, n, m, x, oracle, "double")
