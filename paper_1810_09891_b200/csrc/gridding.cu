@@ -1180,18 +1180,21 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
-      int jb = 0;
-      int4 r = nb > 0 ? rs[0] : make_int4(0, 0, 0, 0);
-      while (jb < nb) {
+      // walk the batch with pointers: node row, sample, record
+      const double* pw = ws;
+      const C* pf = fv;
+      const int4* pr = rs;
+      const int4* const pend = rs + nb;
+      int4 r = nb > 0 ? *pr : make_int4(0, 0, 0, 0);
+      while (pr < pend) {
 #define NFFTK_PIPE_NODE(H)                                                                 \
   if (r.x <= wa_hi && r.x + (int)((unsigned)r.w & 0xffu) > wa_lo) {                        \
     /* halo-indexed factor rows: zero off the stencil, no per-lane test */                  \
-    const double* w = ws + jb * PR;                                                        \
-    const R s = (R)(w[a] * w[H2 + b]);                                                     \
+    const R s = (R)(pw[a] * pw[H2 + b]);                                                   \
     touched = true;                                                                        \
-    const C f = fv[jb];                                                                    \
+    const C f = *pf;                                                                       \
     const R cr = f.x * s, ci = f.y * s;                                                    \
-    const double2* w2 = reinterpret_cast<const double2*>(w + 2 * H2);                     \
+    const double2* w2 = reinterpret_cast<const double2*>(pw + 2 * H2);                    \
     _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                       \
       const double2 v = w2[p];                                                             \
       accr[H + 2 * p] = fma(cr, (R)v.x, accr[H + 2 * p]);                                  \
@@ -1202,17 +1205,23 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }                                                                                    \
     }                                                                                      \
   }
+#define NFFTK_PIPE_NEXT \
+  ++pr;                 \
+  pw += PR;             \
+  ++pf;
 #define NFFTK_PIPE_CASE(H)                                   \
     case H:                                                    \
       if constexpr (H + K <= H2) {                             \
         for (;;) {                                             \
           NFFTK_PIPE_NODE(H)                                   \
-          if (++jb >= nb) break;                               \
-          r = rs[jb];                                          \
+          NFFTK_PIPE_NEXT                                      \
+          if (pr >= pend) break;                               \
+          r = *pr;                                             \
           if (r.z != H) break;                                 \
         }                                                      \
       } else {                                                 \
-        if (++jb < nb) r = rs[jb];                             \
+        NFFTK_PIPE_NEXT                                        \
+        if (pr < pend) r = *pr;                                \
       }                                                        \
       break;
         switch (r.z) {
@@ -1220,10 +1229,12 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
           NFFTK_PIPE_CASE(4) NFFTK_PIPE_CASE(5) NFFTK_PIPE_CASE(6) NFFTK_PIPE_CASE(7)
           NFFTK_PIPE_CASE(8)
           default:
-            if (++jb < nb) r = rs[jb];
+            NFFTK_PIPE_NEXT
+            if (pr < pend) r = *pr;
             break;
         }
 #undef NFFTK_PIPE_CASE
+#undef NFFTK_PIPE_NEXT
 #undef NFFTK_PIPE_NODE
       }
       __syncwarp();
