@@ -141,6 +141,12 @@ int32_t nfftk_trafo_host(int32_t handle, const void * fhat, void * f);
 int32_t nfftk_adjoint_host(int32_t handle, const void * f, void * fhat);
 int32_t nfftk_trafo_device(int32_t handle, const void * fhat_dev, void * f_dev, void * stream);
 int32_t nfftk_adjoint_device(int32_t handle, const void * f_dev, void * fhat_dev, void * stream);
+/* exact sums Plan.ndft / Plan.ndft_adjoint (transform.py:188-234), complex128
+ * interleaved in and out, on the device (cuBLAS ZGEMM over the last dim) */
+int32_t nfftk_ndft_host(int32_t handle, const double * fhat, double * f);
+int32_t nfftk_ndft_adjoint_host(int32_t handle, const double * f, double * fhat);
+int32_t nfftk_ndft_device(int32_t handle, const void * fhat_dev, void * f_dev, void * stream);
+int32_t nfftk_ndft_adjoint_device(int32_t handle, const void * f_dev, void * fhat_dev, void * stream);
 /* adjoint split for multi-GPU: spread into the plan grid, (caller reduces the
  * grid, e.g. NCCL all-reduce on a grid bound with nfftk_bind_grid), finish */
 int32_t nfftk_spread_device(int32_t handle, const void * f_dev, void * stream);

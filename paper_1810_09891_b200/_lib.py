@@ -46,6 +46,10 @@ SIGNATURES = {
     "nfftk_adjoint_host": (_i32, [_i32, _vp, _vp]),
     "nfftk_trafo_device": (_i32, [_i32, _vp, _vp, _vp]),
     "nfftk_adjoint_device": (_i32, [_i32, _vp, _vp, _vp]),
+    "nfftk_ndft_host": (_i32, [_i32, _vp, _vp]),
+    "nfftk_ndft_adjoint_host": (_i32, [_i32, _vp, _vp]),
+    "nfftk_ndft_device": (_i32, [_i32, _vp, _vp, _vp]),
+    "nfftk_ndft_adjoint_device": (_i32, [_i32, _vp, _vp, _vp]),
     "nfftk_spread_device": (_i32, [_i32, _vp, _vp]),
     "nfftk_adjoint_finish_device": (_i32, [_i32, _vp, _vp]),
     "nfftk_bind_grid": (_i32, [_i32, _vp, _i64]),

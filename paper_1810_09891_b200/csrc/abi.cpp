@@ -331,6 +331,30 @@ int32_t nfftk_adjoint_host(int32_t h, const void* f, void* fhat) {
   return guarded(e, [&] { plan_adjoint_host(e->plan, f, fhat); });
 }
 
+int32_t nfftk_ndft_host(int32_t h, const double* fhat, double* f) {
+  Entry* e = lookup(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] { plan_ndft_host(e->plan, fhat, f, false); });
+}
+
+int32_t nfftk_ndft_adjoint_host(int32_t h, const double* f, double* fhat) {
+  Entry* e = lookup(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] { plan_ndft_host(e->plan, f, fhat, true); });
+}
+
+int32_t nfftk_ndft_device(int32_t h, const void* fhat, void* f, void* stream) {
+  Entry* e = lookup(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] { plan_ndft_device(e->plan, fhat, f, false, (cudaStream_t)stream); });
+}
+
+int32_t nfftk_ndft_adjoint_device(int32_t h, const void* f, void* fhat, void* stream) {
+  Entry* e = lookup(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] { plan_ndft_device(e->plan, f, fhat, true, (cudaStream_t)stream); });
+}
+
 int32_t nfftk_trafo_device(int32_t h, const void* fhat, void* f, void* stream) {
   Entry* e = lookup(h);
   if (!e) return ERR_HANDLE;

@@ -13,6 +13,8 @@
 
 #include "plan.h"
 
+#include <cublas_v2.h>
+
 namespace nfftk {
 
 static std::string fmt_tuple(const std::vector<int>& v) {
@@ -108,6 +110,7 @@ std::vector<double> plan_phi_hut(const Plan* p, int dim) {
 Plan::~Plan() {
   if (device >= 0) cudaSetDevice(device);
   if (fft_ready) cufftDestroy(fft);
+  if (cublas) cublasDestroy((cublasHandle_t)cublas);
   cudaFree(x_dev);
   cudaFree(xs);
   cudaFree(perm);

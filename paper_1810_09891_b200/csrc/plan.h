@@ -54,7 +54,8 @@ struct Plan {
   int4* subs = nullptr;
   double* psi = nullptr;
   size_t psi_count = 0;
-  int4* rec = nullptr;              // per-node stencil records, sorted order
+  int4* rec = nullptr;
+  void* cublas = nullptr;            // cublasHandle_t for the exact sums (lazy)              // per-node stencil records, sorted order
   double* lut = nullptr;
   double* cols = nullptr;
   void* grid = nullptr;              // dense n-grid (cuFFT, deconvolution)
@@ -98,6 +99,9 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s);
 void plan_adjoint_finish_device(Plan* p, void* fhat, cudaStream_t s);
 void plan_trafo_host(Plan* p, const void* fhat, void* f);
 void plan_adjoint_host(Plan* p, const void* f, void* fhat);
+// exact sums (ndft.cu), complex128 in and out
+void plan_ndft_device(Plan* p, const void* in, void* out, bool adjoint, cudaStream_t s);
+void plan_ndft_host(Plan* p, const double* in, double* out, bool adjoint);
 void plan_node_order(Plan* p, int64_t* out);
 void plan_bind_grid(Plan* p, void* dev, int64_t bytes);
 void plan_phase_times(Plan* p, double* ms, int64_t* calls, int nmax, int reset);

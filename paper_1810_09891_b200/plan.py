@@ -407,11 +407,39 @@ class Plan:
         self._check(self._lib_checked().nfftk_phase_times(self._h, ms, calls, n, int(bool(reset))))
         return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.PHASES)}
 
+    def _exact(self, data, length, what, outlen, host_fn, dev_fn):
+        lib = self._lib_checked()
+        if not self._params()[7]:
+            raise PlanStateError("plan has no nodes; call set_nodes() first")
+        if _is_torch(data) and data.is_cuda:
+            import torch
+
+            if data.numel() != length or data.dim() < 1:
+                raise ShapeError(f"{what} must have {length} entries, got shape {tuple(data.shape)}")
+            data = data.reshape(length).to(torch.complex128).contiguous()
+            out = torch.empty(outlen, dtype=torch.complex128, device=data.device)
+            self._check(getattr(lib, dev_fn)(self._h, ctypes.c_void_p(data.data_ptr()),
+                                             ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
+            return out
+        out_arr = np.asarray(data)
+        if not (out_arr.shape == (length,) or (out_arr.ndim >= 1 and out_arr.size == length)):
+            raise ShapeError(f"{what} must have {length} entries, got shape {out_arr.shape}")
+        vec = np.ascontiguousarray(out_arr.reshape(length), dtype=np.complex128)
+        out = np.empty(outlen, dtype=np.complex128)
+        self._check(getattr(lib, host_fn)(self._h, vec.ctypes.data, out.ctypes.data))
+        return out
+
     def ndft(self, fhat):
-        raise NotImplementedError("exact NDFT is a test oracle (oracle/), not part of the GPU library")
+        """Exact forward sums f_j = sum_k fhat_k e^{-2 pi i k x_j}, O(M |I_N|)
+        (transform.py:188-203), on the device; complex128 regardless of the
+        plan precision."""
+        return self._exact(fhat, self.num_freqs, "fhat", self.M, "nfftk_ndft_host", "nfftk_ndft_device")
 
     def ndft_adjoint(self, f):
-        raise NotImplementedError("exact NDFT is a test oracle (oracle/), not part of the GPU library")
+        """Exact adjoint sums fhat_k = sum_j f_j e^{+2 pi i k x_j}
+        (transform.py:206-234), on the device; complex128."""
+        return self._exact(f, self.M, "f", self.num_freqs, "nfftk_ndft_adjoint_host",
+                           "nfftk_ndft_adjoint_device")
 
     def __repr__(self):
         return (f"Plan(N={self.N}, M={self.M}, n={self.n}, m={self.m}, "

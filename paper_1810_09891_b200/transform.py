@@ -1,9 +1,9 @@
-"""Module-level transform entry points (reference transform.py:92-176).
+"""Module-level transform entry points (reference transform.py:92-234).
 
 ``trafo(plan, fhat)`` / ``adjoint(plan, f)`` delegate to the plan, which runs
-D -> F -> B (resp. B^H -> F^H -> D^H) on the GPU.  The exact O(M |I_N|) sums
-``ndft`` / ``ndft_adjoint`` of the reference are test oracles and live in
-``oracle/`` (CPU), not in this package.
+D -> F -> B (resp. B^H -> F^H -> D^H) on the GPU.  ``ndft`` / ``ndft_adjoint``
+are the exact O(M |I_N|) sums, also on the GPU (separable phases, one cuBLAS
+ZGEMM over the last dimension per node chunk; csrc/ndft.cu).
 """
 
 
@@ -13,3 +13,13 @@ def trafo(plan, fhat):
 
 def adjoint(plan, f):
     return plan.adjoint(f)
+
+
+def ndft(plan, fhat):
+    """Exact forward sums (transform.py:188-203)."""
+    return plan.ndft(fhat)
+
+
+def ndft_adjoint(plan, f):
+    """Exact adjoint sums (transform.py:206-234)."""
+    return plan.ndft_adjoint(f)
