@@ -242,9 +242,8 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- device-timed region
-    plan.phase_times(reset=True)
-    plan.set_timing(True)
+    # ---- device-timed region (no per-phase instrumentation inside it)
+    plan.set_timing(False)
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -265,6 +264,13 @@ def main():
     torch.cuda.synchronize()
     launches = nf.launch_count() - launches0
     clk = clocks.stop()
+    # ---- the same steps again with per-phase CUDA events (breakdown, roofline)
+    plan.phase_times(reset=True)
+    plan.set_timing(True)
+    for _ in range(args.steps):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
     plan.set_timing(False)
     phases = plan.phase_times(reset=True)
     if world > 1:
