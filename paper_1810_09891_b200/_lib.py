@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnfftk.so")
+# NFFTK_LIB: development override (A/B builds of the same sources, tools/build_variant.sh)
+LIB_PATH = os.environ.get("NFFTK_LIB") or os.path.join(HERE, "libnfftk.so")
 
 _i32, _i64, _u32, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 _vp, _cp, _dp = ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)

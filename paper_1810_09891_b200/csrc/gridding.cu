@@ -332,6 +332,92 @@ __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, 
   }
 }
 
+// Bank-conflict-free row schedule for the d = 3 c128 gather.  A TEAM lane
+// walks whole stencil rows (t0, t1) of 2m cells; one LDS.128 of 32 lanes is
+// served per quarter warp, so the 8 rows a quarter warp reads together must
+// start in 8 different 16-byte bank groups.  Row (t0, t1) starts in group
+// (alpha t0 + beta t1 + corner) mod 8 with alpha = H1 HS, beta = HS (the
+// corner shift is common to the team).  The natural order p = tl + TEAM k
+// wraps t1 at 2m and collides whenever 2m is not a multiple of 8 (m = 5, 6:
+// ~23% extra wavefronts at m = 6); this schedule deals the rows out class by
+// class instead.  Entries are t0 << 8 | t1, 0xffff = no row.
+template <int WF, int TEAM, int H1, int HS>
+struct RowSched {
+  static constexpr int P = WF * WF;
+  static constexpr int NIT = (P + TEAM - 1) / TEAM;
+  unsigned short v[NIT * TEAM];
+  constexpr RowSched() : v() {
+    bool used[P] = {};
+    const int alpha = (H1 * HS) % 8, beta = HS % 8;
+    for (int slot = 0; slot < NIT * TEAM; slot += 8) {  // one quarter warp
+      bool cls[8] = {};
+      for (int l = 0; l < 8; ++l) {
+        int pick = -1;
+        // the unused row of a free class whose class has the most rows left
+        int best = -1;
+        for (int c = 0; c < 8; ++c) {
+          if (cls[c]) continue;
+          int left = 0, first = -1;
+          for (int r = 0; r < P; ++r)
+            if (!used[r] && (alpha * (r / WF) + beta * (r % WF)) % 8 == c) {
+              ++left;
+              if (first < 0) first = r;
+            }
+          if (left > best && first >= 0) {
+            best = left;
+            pick = first;
+          }
+        }
+        if (pick < 0)  // every free class is empty: any unused row (conflict)
+          for (int r = 0; r < P && pick < 0; ++r)
+            if (!used[r]) pick = r;
+        if (pick < 0) {
+          v[slot + l] = 0xffff;
+          continue;
+        }
+        used[pick] = true;
+        cls[(alpha * (pick / WF) + beta * (pick % WF)) % 8] = true;
+        v[slot + l] = (unsigned short)((pick / WF) << 8 | (pick % WF));
+      }
+    }
+  }
+};
+
+template <int WF, int TEAM, int H1, int HS>
+__constant__ RowSched<WF, TEAM, H1, HS> c_row_sched = RowSched<WF, TEAM, H1, HS>();
+
+// One fast (width 2m in every dim) c128 node of the d = 3 gather on the
+// schedule above; sch[] holds this lane's rows.
+template <int MM, int TEAM, int H1, int HS>
+__device__ __forceinline__ void interp_node3_sched(const double2* __restrict__ halo, const int* q,
+                                                   const double* w0, const double* w1,
+                                                   const double* wl, int o0, int o1,
+                                                   const unsigned* sch, double& are, double& aim) {
+  constexpr int WF = 2 * MM;
+  constexpr int NIT = RowSched<WF, TEAM, H1, HS>::NIT;
+  double w2r[WF];
+#pragma unroll
+  for (int t = 0; t < WF; ++t) w2r[t] = wl[t];
+  const double2* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
+#pragma unroll 3
+  for (int k = 0; k < NIT; ++k) {
+    const unsigned e = sch[k];
+    if (e == 0xffffu) continue;
+    const int t0 = e >> 8, t1 = e & 0xff;
+    const double2* row = corner + (t0 * H1 + t1) * HS;
+    double sre = 0, sim = 0;
+#pragma unroll
+    for (int t = 0; t < WF; ++t) {
+      const double2 v = row[t];
+      sre = fma(w2r[t], v.x, sre);
+      sim = fma(w2r[t], v.y, sim);
+    }
+    const double w01 = w0[o0 + t0] * w1[o1 + t1];
+    are = fma(w01, sre, are);
+    aim = fma(w01, sim, aim);
+  }
+}
+
 constexpr int INTERP_NB = 32;
 
 template <typename R, int D, int MM>
@@ -441,6 +527,12 @@ struct IPipeCfg {
   static constexpr int ROWS = H0 * H1;
   static constexpr int THREADS = D == 3 ? 512 : 256;
   static constexpr int TEAM = InterpTeam<D, MM>::value;
+  // conflict-free row schedule: d = 3, c128, 2m not a multiple of 8
+#ifdef NFFTK_NO_SCHED
+  static constexpr bool SCHED = false;
+#else
+  static constexpr bool SCHED = D == 3 && ELEM == 16 && MM > 0 && (2 * MM) % 8 != 0;
+#endif
   static constexpr int NPASS = (32 / TEAM) * (THREADS / 32);  // nodes per CTA pass
   static constexpr int NB = NPASS < 16 ? 16 : (NPASS > 64 ? 64 : NPASS);
   // PRE_PSI row: halo-indexed for d = 3 ([H0 | H1 | 2m+1]), stencil-indexed
@@ -488,6 +580,13 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane % TEAM, sub = lane / TEAM;
   const unsigned halo_tx = (unsigned)(P::ROWS * HS * sizeof(C));
+  constexpr int NIT = P::SCHED ? RowSched<2 * (MM > 0 ? MM : 1), TEAM, H1, HS>::NIT : 1;
+  unsigned sch[NIT];
+  if constexpr (P::SCHED) {
+#pragma unroll
+    for (int k = 0; k < NIT; ++k)
+      sch[k] = c_row_sched<2 * (MM > 0 ? MM : 1), TEAM, H1, HS>.v[k * TEAM + tl];
+  }
   auto issue_halo = [&](int s, int buf) {
     int tc[D];
     tile_of<D>(g, subs[s].x, tc);
@@ -599,7 +698,15 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
         R are = 0, aim = 0;
         if (active) {
           const double* w = ws + jj * PR;
-          if constexpr (D == 3)  // halo-indexed rows [H0 | H1 | 2m+1]
+          if constexpr (D == 3 && P::SCHED) {
+            if (q[6])  // fast node: conflict-free row schedule
+              interp_node3_sched<MM, TEAM, H1, HS>(reinterpret_cast<const double2*>(halo), q, w,
+                                                   w + P::H0, w + P::H0 + P::H1, q[0], q[1], sch,
+                                                   are, aim);
+            else
+              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0],
+                                          q[1], tl, are, aim);
+          } else if constexpr (D == 3)  // halo-indexed rows [H0 | H1 | 2m+1]
             interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0], q[1],
                                         tl, are, aim);
           else  // stencil-indexed rows [2m+1 | 2m+1]

@@ -145,12 +145,16 @@ def test_complex64_configs(cfg, oracle):
 
 # ------------------------------------------------- modes / paths agree
 def test_direct_and_tensor_modes_agree():
-    """kernels.py modes DIRECT and TENSOR use identical factors (SPEC: <= 1e-14)."""
+    """kernels.py modes DIRECT and TENSOR use identical factors (SPEC: <= 1e-14).
+
+    The factors are bitwise identical; the sums are not: the TENSOR gather on
+    the pipelined geometry walks stencil rows in a bank-conflict-free order
+    (gridding.cu RowSched), the DIRECT batch kernel in natural order."""
     c = case("d3_m6")
     a = make_plan(c, psi=nf.MODE_DIRECT)
     b = make_plan(c, psi=nf.MODE_TENSOR)
     assert a.mode == nf.MODE_DIRECT and b.mode == nf.MODE_TENSOR
-    assert np.array_equal(a.trafo(c["fhat"]), b.trafo(c["fhat"]))
+    assert e2(a.trafo(c["fhat"]), b.trafo(c["fhat"])) < 1e-14
     assert e2(a.adjoint(c["f"]), b.adjoint(c["f"])) < 1e-14
 
 
