@@ -222,12 +222,18 @@ def main():
     if args.psi != "flags":
         plan.set_psi_policy(nf.MODE_DIRECT if args.psi == "direct" else nf.MODE_TENSOR)
     x = torch.from_numpy(wl.nodes(w, seed=wl.NODE_SEED + rank)).to(dev)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    dp.set_nodes(x)
-    dp.precompute()
-    torch.cuda.synchronize()
-    precompute_ms = 1000 * (time.perf_counter() - t0)
+    # set_nodes + precompute (sort, stencil records, PRE_PSI): the first call
+    # includes one-time costs (module loading, buffer allocation); the second,
+    # on the same plan, is the steady-state cost the paper reports
+    pre = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dp.set_nodes(x)
+        dp.precompute()
+        torch.cuda.synchronize()
+        pre.append(1000 * (time.perf_counter() - t0))
+    precompute_cold_ms, precompute_ms = pre
     fhat = torch.from_numpy(wl.fhat(w)).to(dev, cdt)
     fsamp = torch.from_numpy(wl.samples(w, seed=wl.F_SEED + rank)).to(dev, cdt)
     f_out = torch.empty(w.M, dtype=cdt, device=dev)
@@ -307,6 +313,7 @@ def main():
         "clocks": clk,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
         "precompute_ms": precompute_ms,
+        "precompute_cold_ms": precompute_cold_ms,
         "fma_peaks_tflops": {"fp64": fp64, "fp32": fp32},
     }
     if world == 1 and not args.no_cpu_baseline:
