@@ -126,6 +126,7 @@ struct Geom {
   int HS;                 // halo row stride (elements) of the last dim
   int nb_spread;          // spread node batch size
   int debug;              // NFFTK_DEBUG bits (experiments only; 0 in production)
+  int dense_flush;        // pipelined c128 spread reduces into the dense grid (periodic wrap per row), no fold
 };
 
 // -------------------------------------------------------- device window

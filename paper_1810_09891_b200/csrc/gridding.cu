@@ -129,6 +129,20 @@ __device__ __forceinline__ void bulk_red_add(void* gdst, const void* ssrc, unsig
                  "r"(smem_u32(ssrc)), "r"(bytes)
                  : "memory");
 }
+// One staged halo row into the DENSE grid: cells [c0, c0 + len) of the row
+// starting at dense index rowbase, c0 in [-n2, n2), wrapped periodically
+// (kernels.py:47 slot arithmetic) -- at most two bulk reductions.  c128 only
+// (every cell a 16-byte unit, so both pieces stay 16-byte aligned).
+template <typename R>
+__device__ __forceinline__ void bulk_red_row_wrapped(cplx_t<R>* grid, int64_t rowbase, int c0, int n2,
+                                                     const cplx_t<R>* src, int len) {
+  const int c = c0 < 0 ? c0 + n2 : c0;
+  const int first = min(len, n2 - c);
+  bulk_red_add<R>(grid + rowbase + c, src, (unsigned)(first * sizeof(cplx_t<R>)));
+  if (first < len)
+    bulk_red_add<R>(grid + rowbase, src + first, (unsigned)((len - first) * sizeof(cplx_t<R>)));
+}
+
 __device__ __forceinline__ void bulk_commit_wait_read() {
   asm volatile("cp.async.bulk.commit_group;\n" ::);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -1375,6 +1389,17 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       fence_proxy_async_smem();
       int tc[3];
       tile_of<3>(g, tile, tc);
+      if constexpr (sizeof(R) == 8) {
+        if (g.dense_flush) {
+          // halo cell (a, b, c) of the tile is dense slot tile * T + (a, b, c) - m
+          int ad = tc[0] * 8 + a - g.m, bd = tc[1] * 8 + b - g.m;
+          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+          bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
+          bulk_red_row_wrapped<R>(gp, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - g.m, g.n[2], dst, H2);
+          asm volatile("cp.async.bulk.commit_group;\n" ::);
+          continue;
+        }
+      }
       int64_t row0 = ((int64_t)(tc[0] * 8 + a) * g.np[1] + tc[1] * 8 + b) * g.np[2] + tc[2] * 8;
       bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
       asm volatile("cp.async.bulk.commit_group;\n" ::);
@@ -1575,8 +1600,19 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       }
       fence_proxy_async_smem();
       const int t0 = tile / g.ntile[1], t1 = tile - t0 * g.ntile[1];
-      int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
-      bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+      bool done = false;
+      if constexpr (sizeof(R) == 8) {
+        if (g.dense_flush) {
+          int ad = t0 * g.T[0] + a - g.m;
+          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+          bulk_red_row_wrapped<R>(gp, (int64_t)ad * g.n[1], t1 * T1 - g.m, g.n[1], dst, H1);
+          done = true;
+        }
+      }
+      if (!done) {
+        int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
+        bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+      }
       asm volatile("cp.async.bulk.commit_group;\n" ::);
     }
   }
@@ -1590,6 +1626,18 @@ bool spread2_pipe_ok(const Geom& g) {
 bool spread_pipe_ok(const Geom& g, int elem_bytes) {
   (void)elem_bytes;
   return g.d == 3 && g.mode == MODE_TENSOR && g.psi && g.rec && g.psi_pad;
+}
+
+// The pipelined c128 spreads can reduce straight into the dense grid (rows
+// wrapped periodically, bulk_red_row_wrapped) instead of the ghost-padded
+// grid + fold: every halo row must fit in one period (H <= n).
+bool spread_dense_ok(const Geom& g, int elem_bytes) {
+  if (elem_bytes != 16 || getenv("NFFTK_NO_DENSE_FLUSH")) return false;
+  const bool pipe = (g.d == 3 && g.m <= 6 && spread_pipe_ok(g, elem_bytes)) || (g.d == 2 && spread2_pipe_ok(g));
+  if (!pipe) return false;
+  for (int i = 0; i < g.d; ++i)
+    if (g.H[i] > g.n[i]) return false;
+  return true;
 }
 
 size_t spread_rr_smem(const Geom& g, int elem_bytes) {

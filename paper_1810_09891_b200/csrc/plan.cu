@@ -585,6 +585,7 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   }
   p->geom.mode = mode;
   p->mode = mode;
+  p->geom.dense_flush = spread_dense_ok(p->geom, p->elem_bytes()) ? 1 : 0;
   ensure_grid(p);
   NFFTK_CUDA(cudaStreamSynchronize(s));
   p->ready = true;
@@ -629,12 +630,17 @@ void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
 void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
-  { PhaseScope ps(p, PH_ZERO, s); NFFTK_CUDA(cudaMemsetAsync(p->gp, 0, p->gp_bytes, s)); }
+  // dense flush: the pipelined spread reduces into the dense grid directly
+  // (periodic wrap per halo row), so there is no ghost-padded grid to fold
+  const bool dense = p->geom.dense_flush != 0;
+  void* target = dense ? p->grid : p->gp;
+  { PhaseScope ps(p, PH_ZERO, s);
+    NFFTK_CUDA(cudaMemsetAsync(target, 0, dense ? p->elem_bytes() * (size_t)p->grid_size : p->gp_bytes, s)); }
   if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * (p->M + 2)));  // +2: aligned bulk copies
   { PhaseScope ps(p, PH_PERMUTE, s); launch_permute(p->single, f, p->perm, p->M, p->f_sorted, s); }
   { PhaseScope ps(p, PH_SPREAD, s);
-    launch_spread(p->single, p->gp, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
-  { PhaseScope ps(p, PH_FOLD, s); launch_fold(p->single, p->gp, p->grid, p->pq, s); }
+    launch_spread(p->single, target, f, p->f_sorted, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+  if (!dense) { PhaseScope ps(p, PH_FOLD, s); launch_fold(p->single, p->gp, p->grid, p->pq, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }
