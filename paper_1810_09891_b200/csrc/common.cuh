@@ -127,6 +127,7 @@ struct Geom {
   int nb_spread;          // spread node batch size
   int debug;              // NFFTK_DEBUG bits (experiments only; 0 in production)
   int dense_flush;        // pipelined c128 spread reduces into the dense grid (periodic wrap per row), no fold
+  int psi_f32;            // PRE_PSI rows stored as fp32 (c64 plans on the pipelined geometries); psi then points at floats
 };
 
 // -------------------------------------------------------- device window
@@ -202,6 +203,14 @@ __host__ __device__ inline int psi_row_halo(int d, const int* H, int K) {
   int s = K;
   for (int i = 0; i + 1 < d; ++i) s += H[i];
   return (s + 1) & ~1;
+}
+
+// PRE_PSI row stride in elements of the factor type: 16-byte rows (fp64
+// factors for c128 plans, fp32 factors for c64 plans on the pipelined
+// geometries, Geom::psi_f32).
+template <typename W>
+__host__ __device__ constexpr int psi_row_pad(int count) {
+  return sizeof(W) == 8 ? (count + 1) & ~1 : (count + 3) & ~3;
 }
 
 template <typename R> struct Cplx;

@@ -260,10 +260,10 @@ struct InterpTeam {
 // leading dim 0 / 1 is w0[o0 + t] / w1[o1 + t] (o = 0 for stencil-indexed
 // rows, the stencil start h for halo-indexed PRE_PSI rows); wl holds the
 // last-dim factors.
-template <typename R, int D, int MM, int TEAM>
+template <typename R, int D, int MM, int TEAM, typename W>
 __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, int HS, int H1, int K,
-                                            const int* q, const double* w0, const double* w1,
-                                            const double* wl, int o0, int o1, int tl, R& are,
+                                            const int* q, const W* w0, const W* w1,
+                                            const W* wl, int o0, int o1, int tl, R& are,
                                             R& aim) {
   using C = cplx_t<R>;
   if (MM > 0 && q[2 * D]) {
@@ -551,9 +551,12 @@ struct IPipeCfg {
   static constexpr int NB = NPASS < 16 ? 16 : (NPASS > 64 ? 64 : NPASS);
   // PRE_PSI row: halo-indexed for d = 3 ([H0 | H1 | 2m+1]), stencil-indexed
   // for d = 2 ([2m+1 | 2m+1]; halo-indexed rows would cost bytes there)
-  static constexpr int PR = D == 3 ? (H0 + H1 + K + 1) & ~1 : 2 * K;
+  // factor type: fp64 rows for c128, fp32 rows for c64 (k_build_psi<float>),
+  // each row padded to 16 bytes
+  using W = R;
+  static constexpr int PR = psi_row_pad<W>(D == 3 ? H0 + H1 + K : 2 * K);
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
-  static constexpr size_t W_BYTES = al(sizeof(double) * NB * PR);
+  static constexpr size_t W_BYTES = al(sizeof(W) * NB * PR);
   static constexpr size_t R_BYTES = al(16 * (size_t)NB);
   static constexpr size_t SB = W_BYTES + R_BYTES + al(4 * (size_t)(NB + 4));
   static constexpr size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
@@ -646,9 +649,9 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     mt->last = pbase + nb >= pend;
     mt->poff = poff;
     unsigned char* st = smem + slot * P::SB;
-    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb, pb = 4u * pcnt;
+    const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb, pb = 4u * pcnt;
     mbar_expect_tx(full + slot, wb + rb + pb);
-    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, perm + (pbase - poff), pb, full + slot);
     if (pbase + nb < pend) {
@@ -686,7 +689,7 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
       mbar_wait(full + slot, (k / S) & 1);
       const StageMetaI mt = meta[slot];
       const unsigned char* st = smem + slot * P::SB;
-      const double* ws = reinterpret_cast<const double*>(st);
+      const typename P::W* ws = reinterpret_cast<const typename P::W*>(st);
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const int* pv = reinterpret_cast<const int*>(st + P::W_BYTES + P::R_BYTES) + mt.poff;
       for (int j0 = warp * NPW; j0 < mt.nb; j0 += NW * NPW) {
@@ -711,7 +714,7 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
         }
         R are = 0, aim = 0;
         if (active) {
-          const double* w = ws + jj * PR;
+          const typename P::W* w = ws + jj * PR;
           if constexpr (D == 3 && P::SCHED) {
             if (q[6])  // fast node: conflict-free row schedule
               interp_node3_sched<MM, TEAM, H1, HS>(reinterpret_cast<const double2*>(halo), q, w,
@@ -1164,10 +1167,11 @@ struct PipeCfg {
   static constexpr int ROWS = H * H;
   static constexpr int THREADS = (ROWS + 31) / 32 * 32;
   static constexpr int BLOCKS = THREADS * 2 * 102 <= 65536 && MM <= 4 ? 2 : 1;
-  static constexpr int PR = (2 * H + K + 1) & ~1;  // halo-indexed PRE_PSI row [H | H | 2m+1]
+  using W = R;                                          // factor type (fp32 rows for c64)
+  static constexpr int PR = psi_row_pad<W>(2 * H + K);  // halo-indexed PRE_PSI row [H | H | 2m+1]
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
   static constexpr size_t stage_bytes(int nb) {
-    return al(sizeof(double) * nb * PR) + al(16 * (size_t)nb) + al((size_t)ELEM * (nb + 2));
+    return al(sizeof(W) * nb * PR) + al(16 * (size_t)nb) + al((size_t)ELEM * (nb + 2));
   }
   static constexpr size_t rows_bytes = al((size_t)ROWS * HS * ELEM);
   static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMeta) * s + 32); }
@@ -1188,7 +1192,7 @@ struct PipeCfg {
   static constexpr int NB = pick_nb();
   static constexpr int S = pick_s();
   static constexpr size_t SB = stage_bytes(NB > 0 ? NB : 1);
-  static constexpr size_t W_BYTES = al(sizeof(double) * (NB > 0 ? NB : 1) * PR);
+  static constexpr size_t W_BYTES = al(sizeof(W) * (NB > 0 ? NB : 1) * PR);
   static constexpr size_t R_BYTES = al(16 * (size_t)(NB > 0 ? NB : 1));
   static constexpr size_t CTL = (S > 0 ? S : 1) * SB;    // control block offset
   static constexpr size_t ROWS_OFF = CTL + ctl_bytes(S > 0 ? S : 1);
@@ -1252,10 +1256,10 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     mt->last = pbase + nb >= pend;
     mt->foff = foff;
     unsigned char* st = smem + slot * P::SB;
-    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb,
+    const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb,
                    fb = (unsigned)sizeof(C) * fcnt;
     mbar_expect_tx(full + slot, wb + rb + fb);
-    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
     if (pbase + nb < pend) {
@@ -1297,12 +1301,12 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       if (mt.nb < 0) break;
       tile = mt.tile;
       const unsigned char* st = smem + slot * P::SB;
-      const double* ws = reinterpret_cast<const double*>(st);
+      const typename P::W* ws = reinterpret_cast<const typename P::W*>(st);
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
       // walk the batch with pointers: node row, sample, record
-      const double* pw = ws;
+      const typename P::W* pw = ws;
       const C* pf = fv;
       const int4* pr = rs;
       const int4* const pend = rs + nb;
@@ -1315,9 +1319,9 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     touched = true;                                                                        \
     const C f = *pf;                                                                       \
     const R cr = f.x * s, ci = f.y * s;                                                    \
-    const double2* w2 = reinterpret_cast<const double2*>(pw + 2 * H2);                    \
+    const C* w2 = reinterpret_cast<const C*>(pw + 2 * H2); /* factor pairs */             \
     _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                       \
-      const double2 v = w2[p];                                                             \
+      const C v = w2[p];                                                                   \
       accr[H + 2 * p] = fma(cr, (R)v.x, accr[H + 2 * p]);                                  \
       acci[H + 2 * p] = fma(ci, (R)v.x, acci[H + 2 * p]);                                  \
       if (2 * p + 1 < K) {                                                                 \
@@ -1422,11 +1426,12 @@ struct Pipe2Cfg {
   static constexpr int H1 = T1 + K;
   static constexpr int ELEM = 2 * (int)sizeof(R);
   static constexpr int HS = ELEM == 8 ? H1 + (H1 & 1) : H1;  // 16-byte rows
-  static constexpr int PR = 2 * K;                            // stencil-indexed PRE_PSI row
+  using W = R;                                                // factor type (fp32 rows for c64)
+  static constexpr int PR = psi_row_pad<W>(2 * K);            // stencil-indexed PRE_PSI row
   static constexpr int NB = 16;
   static constexpr int S = 4;
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
-  static constexpr size_t W_BYTES = al(sizeof(double) * NB * PR);
+  static constexpr size_t W_BYTES = al(sizeof(W) * NB * PR);
   static constexpr size_t R_BYTES = al(16 * (size_t)NB);
   static constexpr size_t SB = W_BYTES + R_BYTES + al((size_t)ELEM * (NB + 2));
   static constexpr size_t CTL = S * SB;
@@ -1485,10 +1490,10 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     mt->last = pbase + nb >= pend;
     mt->foff = foff;
     unsigned char* st = smem + slot * P::SB;
-    const unsigned wb = (unsigned)(sizeof(double) * PR) * nb, rb = 16u * nb,
+    const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb,
                    fb = (unsigned)sizeof(C) * fcnt;
     mbar_expect_tx(full + slot, wb + rb + fb);
-    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
+    bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
     if (pbase + nb < pend) {
@@ -1522,7 +1527,7 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       if (mt.nb < 0) break;
       tile = mt.tile;
       const unsigned char* st = smem + slot * P::SB;
-      const double* ws = reinterpret_cast<const double*>(st);
+      const typename P::W* ws = reinterpret_cast<const typename P::W*>(st);
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
@@ -1533,12 +1538,12 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
   {                                                                                        \
     const int ta = a - r.x;                                                                \
     const bool act = (unsigned)ta < ((unsigned)r.w & 0xffu);                               \
-    const double* w = ws + jb * PR;                                                        \
-    const double s0 = w[min((unsigned)ta, (unsigned)(K - 1))];                             \
+    const typename P::W* w = ws + jb * PR;                                                 \
+    const typename P::W s0 = w[min((unsigned)ta, (unsigned)(K - 1))];                      \
     const R s = act ? (R)s0 : (R)0;                                                        \
     const C f = fv[jb];                                                                    \
     const R cr = f.x * s, ci = f.y * s;                                                    \
-    const double* w1 = w + K;                                                              \
+    const typename P::W* w1 = w + K;                                                       \
     _Pragma("unroll") for (int t = 0; t < K; ++t) {                                        \
       accr[H + t] = fma(cr, (R)w1[t], accr[H + t]);                                        \
       acci[H + t] = fma(ci, (R)w1[t], acci[H + t]);                                        \

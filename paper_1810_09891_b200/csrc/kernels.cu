@@ -114,8 +114,9 @@ __global__ void k_sum_widths(const double* __restrict__ xs, int64_t M, Geom g,
 }
 
 // PRE_PSI table (kernels.py:56-72), sorted node order, zero-filled past width.
+template <typename T>
 __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
-                            double* __restrict__ psi) {
+                            T* __restrict__ psi) {
   const int K = 2 * g.m + 1, pr = g.pr;
   const int64_t total = M * pr;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
@@ -148,12 +149,17 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
         continue;
       }
     }
-    psi[q] = t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0;
+    // factors are evaluated in fp64 (window.py:56-72) and rounded once to
+    // the table type
+    psi[q] = (T)(t < st.width ? dim_factor(g, dim, x, st.lo + t) * g.wscale[dim] : 0.0);
   }
 }
 
-void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s) {
-  k_build_psi<<<blocks_for(M * g.pr, 256), 256, 0, s>>>(xs, M, g, psi);
+void build_psi(const double* xs, int64_t M, const Geom& g, void* psi, cudaStream_t s) {
+  if (g.psi_f32)
+    k_build_psi<float><<<blocks_for(M * g.pr, 256), 256, 0, s>>>(xs, M, g, (float*)psi);
+  else
+    k_build_psi<double><<<blocks_for(M * g.pr, 256), 256, 0, s>>>(xs, M, g, (double*)psi);
   count_launch();
 }
 

@@ -33,7 +33,7 @@ void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int
                   int* perm, double* xs, int* tile_count, int* tile_start, int4** subs,
                   int* nsubs, cudaStream_t s);
 unsigned long long sum_widths(const double* xs, int64_t M, const Geom& g, cudaStream_t s);
-void build_psi(const double* xs, int64_t M, const Geom& g, double* psi, cudaStream_t s);
+void build_psi(const double* xs, int64_t M, const Geom& g, void* psi, cudaStream_t s);
 bool pipe_geometry(const Geom& g);
 bool spread_dense_ok(const Geom& g, int elem_bytes);
 void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, cudaStream_t s);

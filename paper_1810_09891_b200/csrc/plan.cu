@@ -568,12 +568,27 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   p->geom.mode = MODE_DIRECT;  // psi table itself is built from exact factors
   p->geom.psi = nullptr;
   p->geom.psi_pad = 0;
+  p->geom.psi_f32 = 0;
   p->geom.pr = psi_row(p->d, 2 * p->m + 1);
   if (mode == MODE_TENSOR) {
     p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? 1 : 0;
     p->geom.pr = p->geom.psi_pad ? psi_row_halo(p->d, p->geom.H, 2 * p->m + 1)
                                  : psi_row(p->d, 2 * p->m + 1);
-    size_t count = (size_t)p->M * p->geom.pr;
+    // c64 plans on the pipelined geometries (only the pipelined kernels read
+    // the table there) keep fp32 factor rows: half the bytes, no per-FMA
+    // fp64 -> fp32 conversions
+    if (p->single && pipe_geometry(p->geom)) {
+      p->geom.psi_f32 = 1;
+      int s0 = 2 * p->m + 1;
+      if (p->geom.psi_pad)
+        for (int i = 0; i + 1 < p->d; ++i) s0 += p->geom.H[i];
+      else
+        s0 = p->d * (2 * p->m + 1);
+      p->geom.pr = psi_row_pad<float>(s0);
+    }
+    const size_t esz = p->geom.psi_f32 ? sizeof(float) : sizeof(double);
+    // psi_count counts doubles of storage
+    size_t count = ((size_t)p->M * p->geom.pr * esz + sizeof(double) - 1) / sizeof(double);
     if (p->psi && count != p->psi_count) {
       cudaFree(p->psi);
       p->psi = nullptr;
