@@ -131,8 +131,9 @@ __device__ __forceinline__ void bulk_red_add(void* gdst, const void* ssrc, unsig
 }
 // One staged halo row into the DENSE grid: cells [c0, c0 + len) of the row
 // starting at dense index rowbase, c0 in [-n2, n2), wrapped periodically
-// (kernels.py:47 slot arithmetic) -- at most two bulk reductions.  c128 only
-// (every cell a 16-byte unit, so both pieces stay 16-byte aligned).
+// (kernels.py:47 slot arithmetic) -- at most two bulk reductions.  Both
+// pieces stay 16-byte aligned: c128 cells are 16 bytes; c64 needs c0, len
+// and n2 even (spread_dense_ok).
 template <typename R>
 __device__ __forceinline__ void bulk_red_row_wrapped(cplx_t<R>* grid, int64_t rowbase, int c0, int n2,
                                                      const cplx_t<R>* src, int len) {
@@ -1393,16 +1394,15 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       fence_proxy_async_smem();
       int tc[3];
       tile_of<3>(g, tile, tc);
-      if constexpr (sizeof(R) == 8) {
-        if (g.dense_flush) {
-          // halo cell (a, b, c) of the tile is dense slot tile * T + (a, b, c) - m
-          int ad = tc[0] * 8 + a - g.m, bd = tc[1] * 8 + b - g.m;
-          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
-          bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
-          bulk_red_row_wrapped<R>(gp, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - g.m, g.n[2], dst, H2);
-          asm volatile("cp.async.bulk.commit_group;\n" ::);
-          continue;
-        }
+      if (g.dense_flush) {
+        // halo cell (a, b, c) of the tile is dense slot tile * T + (a, b, c) - m;
+        // the row goes out as HS cells (c64: one trailing zero keeps 16 bytes)
+        int ad = tc[0] * 8 + a - g.m, bd = tc[1] * 8 + b - g.m;
+        ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+        bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
+        bulk_red_row_wrapped<R>(gp, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - g.m, g.n[2], dst, HS);
+        asm volatile("cp.async.bulk.commit_group;\n" ::);
+        continue;
       }
       int64_t row0 = ((int64_t)(tc[0] * 8 + a) * g.np[1] + tc[1] * 8 + b) * g.np[2] + tc[2] * 8;
       bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
@@ -1606,13 +1606,11 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       fence_proxy_async_smem();
       const int t0 = tile / g.ntile[1], t1 = tile - t0 * g.ntile[1];
       bool done = false;
-      if constexpr (sizeof(R) == 8) {
-        if (g.dense_flush) {
-          int ad = t0 * g.T[0] + a - g.m;
-          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
-          bulk_red_row_wrapped<R>(gp, (int64_t)ad * g.n[1], t1 * T1 - g.m, g.n[1], dst, H1);
-          done = true;
-        }
+      if (g.dense_flush) {
+        int ad = t0 * g.T[0] + a - g.m;
+        ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+        bulk_red_row_wrapped<R>(gp, (int64_t)ad * g.n[1], t1 * T1 - g.m, g.n[1], dst, HS);
+        done = true;
       }
       if (!done) {
         int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
@@ -1637,12 +1635,15 @@ bool spread_pipe_ok(const Geom& g, int elem_bytes) {
 // wrapped periodically, bulk_red_row_wrapped) instead of the ghost-padded
 // grid + fold: every halo row must fit in one period (H <= n).
 bool spread_dense_ok(const Geom& g, int elem_bytes) {
-  if (elem_bytes != 16 || getenv("NFFTK_NO_DENSE_FLUSH")) return false;
+  if (getenv("NFFTK_NO_DENSE_FLUSH")) return false;
+  // c64: 8-byte cells, so the row start (tile * 8 - m), the staged row (HS,
+  // even) and the period must all be even to keep 16-byte bulk reductions
+  if (elem_bytes == 8 && (g.m % 2 != 0 || g.n[g.d - 1] % 2 != 0 || g.HS % 2 != 0)) return false;
   const bool pipe = (g.d == 3 && g.m <= 6 && spread_pipe_ok(g, elem_bytes)) || (g.d == 2 && spread2_pipe_ok(g));
   if (!pipe) return false;
   for (int i = 0; i < g.d; ++i)
     if (g.H[i] > g.n[i]) return false;
-  return true;
+  return g.HS <= g.n[g.d - 1];
 }
 
 size_t spread_rr_smem(const Geom& g, int elem_bytes) {
