@@ -433,6 +433,42 @@ __device__ __forceinline__ void interp_node3_sched(const double2* __restrict__ h
   }
 }
 
+// One fast c64 node of the d = 3 gather.  c64 halo rows have an even stride
+// (HS = H + 1 keeps TMA rows 16-byte), so whole-row lanes start in only half
+// of the 8-byte bank pairs; here a TEAM of 16 is 8 row slots x 2 parities:
+// the two lanes of a slot read the even / odd cells of one row, and the 8
+// rows a half warp reads together come from RowSched over 16-byte units
+// (HS / 2), so the 16 lanes hit 16 different bank pairs.
+template <int MM, int H1, int HS>
+__device__ __forceinline__ void interp_node3_half(const float2* __restrict__ halo, const int* q,
+                                                  const float* w0, const float* w1,
+                                                  const float* wl, int o0, int o1, int par,
+                                                  const unsigned* sch, float& are, float& aim) {
+  constexpr int WF = 2 * MM;
+  constexpr int NIT = RowSched<WF, 8, H1, HS / 2>::NIT;
+  float w2r[MM];
+#pragma unroll
+  for (int t = 0; t < MM; ++t) w2r[t] = wl[2 * t + par];
+  const float2* corner = halo + (q[0] * H1 + q[1]) * HS + q[2] + par;
+#pragma unroll 3
+  for (int k = 0; k < NIT; ++k) {
+    const unsigned e = sch[k];
+    if (e == 0xffffu) continue;
+    const int t0 = e >> 8, t1 = e & 0xff;
+    const float2* row = corner + (t0 * H1 + t1) * HS;
+    float sre = 0, sim = 0;
+#pragma unroll
+    for (int t = 0; t < MM; ++t) {
+      const float2 v = row[2 * t];
+      sre = fmaf(w2r[t], v.x, sre);
+      sim = fmaf(w2r[t], v.y, sim);
+    }
+    const float w01 = w0[o0 + t0] * w1[o1 + t1];
+    are = fmaf(w01, sre, are);
+    aim = fmaf(w01, sim, aim);
+  }
+}
+
 constexpr int INTERP_NB = 32;
 
 template <typename R, int D, int MM>
@@ -541,7 +577,14 @@ struct IPipeCfg {
   static constexpr int HS = ELEM == 8 ? HL + (HL & 1) : HL;
   static constexpr int ROWS = H0 * H1;
   static constexpr int THREADS = D == 3 ? 512 : 256;
-  static constexpr int TEAM = InterpTeam<D, MM>::value;
+  // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
+#ifdef NFFTK_NO_HALF
+  static constexpr bool HALF = false;
+#else
+  // HS / 2 = m + 5 must be odd; below m = 6 the half rows are too short to pay (C5 c64: 16.6 -> 21.2 ms)
+  static constexpr bool HALF = D == 3 && ELEM == 8 && MM >= 6 && (MM % 2 == 0);
+#endif
+  static constexpr int TEAM = HALF ? 16 : InterpTeam<D, MM>::value;
   // conflict-free row schedule: d = 3, c128, 2m not a multiple of 8
 #ifdef NFFTK_NO_SCHED
   static constexpr bool SCHED = false;
@@ -598,12 +641,18 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane % TEAM, sub = lane / TEAM;
   const unsigned halo_tx = (unsigned)(P::ROWS * HS * sizeof(C));
-  constexpr int NIT = P::SCHED ? RowSched<2 * (MM > 0 ? MM : 1), TEAM, H1, HS>::NIT : 1;
+  constexpr int NIT = P::SCHED  ? RowSched<2 * (MM > 0 ? MM : 1), TEAM, H1, HS>::NIT
+                     : P::HALF ? RowSched<2 * (MM > 0 ? MM : 1), 8, H1, HS / 2>::NIT
+                               : 1;
   unsigned sch[NIT];
   if constexpr (P::SCHED) {
 #pragma unroll
     for (int k = 0; k < NIT; ++k)
       sch[k] = c_row_sched<2 * (MM > 0 ? MM : 1), TEAM, H1, HS>.v[k * TEAM + tl];
+  } else if constexpr (P::HALF) {
+#pragma unroll
+    for (int k = 0; k < NIT; ++k)
+      sch[k] = c_row_sched<2 * (MM > 0 ? MM : 1), 8, H1, HS / 2>.v[k * 8 + (tl >> 1)];
   }
   auto issue_halo = [&](int s, int buf) {
     int tc[D];
@@ -721,6 +770,13 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
               interp_node3_sched<MM, TEAM, H1, HS>(reinterpret_cast<const double2*>(halo), q, w,
                                                    w + P::H0, w + P::H0 + P::H1, q[0], q[1], sch,
                                                    are, aim);
+            else
+              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0],
+                                          q[1], tl, are, aim);
+          } else if constexpr (D == 3 && P::HALF) {
+            if (q[6])  // fast node: half-row lanes on the conflict-free schedule
+              interp_node3_half<MM, H1, HS>(reinterpret_cast<const float2*>(halo), q, w, w + P::H0,
+                                            w + P::H0 + P::H1, q[0], q[1], tl & 1, sch, are, aim);
             else
               interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0],
                                           q[1], tl, are, aim);
