@@ -99,3 +99,23 @@ def test_pipe_dense_cell_many_subproblems(d, oracle, monkeypatch):
     x = nodes(d, n, 5000, seed=3, kind="dense")
     p = plan(N, n, m, x, "double", monkeypatch, tile=8 if d == 3 else None)
     check(p, N, n, m, x, oracle, "double")
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("d,m", [(3, 4), (3, 5), (3, 6), (2, 4), (2, 6)])
+def test_dense_flush_matches_padded_fold(d, m, precision, oracle, monkeypatch):
+    """The pipelined spreads reduce straight into the dense grid (rows
+    wrapped periodically; c64 only for even m) -- same adjoint as the
+    ghost-padded grid + fold path (NFFTK_NO_DENSE_FLUSH) and as the oracle,
+    with nodes on every periodic boundary."""
+    N, n = ((16, 16, 16), (32, 32, 32)) if d == 3 else ((32, 32), (64, 64))
+    x = nodes(d, n, 4000, seed=20 + m, kind="edges")
+    rng = np.random.default_rng(5)
+    fs = rng.standard_normal(x.shape[0]) + 1j * rng.standard_normal(x.shape[0])
+    dense = plan(N, n, m, x, precision, monkeypatch, tile=8 if d == 3 else None)
+    monkeypatch.setenv("NFFTK_NO_DENSE_FLUSH", "1")
+    padded = plan(N, n, m, x, precision, monkeypatch, tile=8 if d == 3 else None)
+    monkeypatch.delenv("NFFTK_NO_DENSE_FLUSH")
+    a, b = dense.adjoint(fs), padded.adjoint(fs)
+    assert e2(b, a) < (1e-14 if precision == "double" else 1e-6)
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
