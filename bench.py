@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(wl.CONFIGS))
     ap.add_argument("--precision", default="double", choices=["double", "single"])
     ap.add_argument("--psi", default="flags", choices=["flags", "direct", "tensor"])
+    ap.add_argument("--reduce", default="fhat", choices=["fhat", "grid"],
+                    help="adjoint exchange at N>1: all-reduce the coefficients or the n-grid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -65,6 +67,8 @@ def config_json(w, args, world):
         "nodes": w.dist, "window": "kaiserbessel", "flags": "default f1 (PRE_PHI_HUT|PRE_PSI|sort)"
         if args.psi == "flags" else f"psi={args.psi}",
         "step": "trafo + adjoint", "parallelism": f"node-sharded x{world}",
+        "adjoint_exchange": "none (1 rank)" if world == 1 else
+        f"NCCL all-reduce of the {'coefficients (|I_N|)' if args.reduce == 'fhat' else 'n-grid (|I_n|)'}",
         "l2": "flushed (256 MiB write) before every timed step",
     }
 
@@ -217,7 +221,8 @@ def main():
     s_elem = 8 if args.precision == "single" else 16
 
     # ---- plan over this rank's shard (weak scaling: M nodes per rank)
-    dp = DistributedPlan(w.N, w.M, n=w.n, m=w.m, precision=args.precision, device=dev)
+    dp = DistributedPlan(w.N, w.M, n=w.n, m=w.m, precision=args.precision, device=dev,
+                         reduce=args.reduce)
     plan = dp.plan
     if args.psi != "flags":
         plan.set_psi_policy(nf.MODE_DIRECT if args.psi == "direct" else nf.MODE_TENSOR)

@@ -43,7 +43,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, reduce, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -55,7 +55,7 @@ def _worker(rank, world, port, case, q):
         fh = rng.standard_normal(K) + 1j * rng.standard_normal(K)
         f = rng.standard_normal(M) + 1j * rng.standard_normal(M)
         lo, hi = shard_bounds(M, world, rank)
-        eng = DistributedNfft(OracleEngine(N, n, m, x[lo:hi]))
+        eng = DistributedNfft(OracleEngine(N, n, m, x[lo:hi]), reduce=reduce)
         f_loc = eng.trafo(torch.from_numpy(fh))
         a = eng.adjoint(torch.from_numpy(f[lo:hi]))
         q.put((rank, lo, f_loc.numpy(), a.numpy()))
@@ -68,14 +68,15 @@ def _worker(rank, world, port, case, q):
 
 @pytest.mark.parametrize("case", [((16,), (32,), 4, 101), ((8, 8), (16, 20), 3, 333),
                                   ((8, 8, 8), (16, 16, 16), 3, 257)])
-def test_sharded_trafo_adjoint_world2(case):
+@pytest.mark.parametrize("reduce", ["fhat", "grid"])
+def test_sharded_trafo_adjoint_world2(case, reduce):
     from oracle import oracle as O
 
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, reduce, q)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=180) for _ in range(world)]
@@ -107,3 +108,8 @@ def test_shard_bounds_partition():
             assert all(spans[r][1] == spans[r + 1][0] for r in range(world - 1))
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_reduce_mode_validated():
+    with pytest.raises(ValueError):
+        DistributedNfft(object(), reduce="slab")
