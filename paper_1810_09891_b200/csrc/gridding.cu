@@ -1624,7 +1624,10 @@ struct Pipe2Cfg {
   using W = R;                                                // factor type (fp32 rows for c64)
   static constexpr int PR = psi_row_pad<W>(2 * K);            // stencil-indexed PRE_PSI row
   static constexpr int NB = 16;
-  static constexpr int S = 4;
+  // ring depth: measured at C4 (A/B, tools/ab_c4.sh) -- 3 stages for fp32
+  // (spread 1.85 -> 1.71 ms: smaller CTAs, more of them per SM), 4 for fp64
+  // (3 stages: 2.86 -> 3.29 ms)
+  static constexpr int S = sizeof(R) == 4 ? 3 : 4;
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
   static constexpr size_t W_BYTES = al(sizeof(W) * NB * PR);
   static constexpr size_t R_BYTES = al(16 * (size_t)NB);
