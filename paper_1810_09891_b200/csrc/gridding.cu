@@ -1223,13 +1223,19 @@ struct PipeCfg {
   static constexpr int ELEM = 2 * (int)sizeof(R);        // complex element bytes
   static constexpr int HS = ELEM == 8 ? H + 1 : H;       // row stride (Geom::HS)
   static constexpr int ROWS = H * H;
-  static constexpr int THREADS = (ROWS + 31) / 32 * 32;
+#ifndef NFFTK_RPT
+#define NFFTK_RPT 1
+#endif
+  static constexpr int RPT = sizeof(R) == 8 ? NFFTK_RPT : 1;  // rows per thread (run-window path)
+  static constexpr int HB = (H + RPT - 1) / RPT;              // row groups per a-line
+  static constexpr int GROUPS = H * HB;
+  static constexpr int THREADS = (GROUPS + 31) / 32 * 32;
   static constexpr int BLOCKS = THREADS * 2 * 102 <= 65536 && MM <= 4 ? 2 : 1;
   // Register budget of 2 CTAs/SM: run-window accumulators (K cells, the
   // factor loads of a node all in flight) instead of the whole halo row
   // (measured C5 spread 52.2 -> 41.8 ms; the whole-row switch stays 5% faster
   // at m = 6 (1 CTA/SM, 128 registers) and 3% faster for fp32 rows).
-  static constexpr bool RUNACC = BLOCKS == 2 && sizeof(R) == 8;
+  static constexpr bool RUNACC = (BLOCKS == 2 || RPT > 1) && sizeof(R) == 8;
   using W = R;                                          // factor type (fp32 rows for c64)
   static constexpr int PR = psi_row_pad<W>(2 * H + K);  // halo-indexed PRE_PSI row [H | H | 2m+1]
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
@@ -1345,65 +1351,81 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   // (warp-uniformly) the nodes whose stencil misses them -- measured 12%
   // faster than strided ownership, where every warp sees every node.
   // Non-owners get an out-of-range row so the stencil test never passes.
-  const int row = threadIdx.x;
-  const bool owner = row < P::ROWS;  // non-owners accumulate garbage that is never flushed
-  const int a = owner ? row / H2 : 0, b = owner ? row % H2 : 0;
-  const int wa_lo = min((int)(threadIdx.x & ~31u), P::ROWS - 1) / H2;
-  const int wa_hi = min((int)(threadIdx.x | 31u), P::ROWS - 1) / H2;
   int k = 0;
   if constexpr (P::RUNACC) {
   // Run accumulators: the K cells a run of equal last-dim start touches stay
-  // in registers (static indices, no switch); at the end of a run they are
-  // added into this thread's own shared-memory row (no other thread touches
-  // it: no atomics, no conflicts).  [lo_w, hi_w) is the written part of the
-  // row; cells outside it are stored instead of added, so the row needs no
-  // zeroing, and only the written part is bulk-reduced at the end of a tile.
-  C* const myrow = stage + (size_t)row * HS;
+  // in registers (static indices, no switch); when the run start moves they
+  // go to this thread's own shared-memory rows (no other thread touches
+  // them: no atomics, no conflicts).  A thread owns RPT rows (a, b0 + j) of
+  // one a-line, so one set of factor loads feeds RPT rows and fewer warps
+  // walk each node.  [lo_w, hi_w) is the written part of the rows; cells
+  // outside it are stored instead of added, so the rows need no zeroing, and
+  // only the written part is bulk-reduced at the end of a tile.
+  constexpr int RPT = P::RPT, HB = P::HB;
+  const int grp = threadIdx.x;
+  const bool gown = grp < P::GROUPS;  // padding threads own no row
+  const int a = gown ? grp / HB : 0, b0 = gown ? (grp % HB) * RPT : 0;
+  const int wa_lo = min((int)(threadIdx.x & ~31u), P::GROUPS - 1) / HB;
+  const int wa_hi = min((int)(threadIdx.x | 31u), P::GROUPS - 1) / HB;
+  C* const myrow = stage + (size_t)(a * H2 + b0) * HS;  // row j at myrow + j * HS
+  auto owns = [&](int j) { return gown && b0 + j < H2; };
   for (;;) {  // tiles of this CTA
-    R accr[K], acci[K];
+    R accr[RPT][K], acci[RPT][K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) accr[c] = acci[c] = 0;
+    for (int j = 0; j < RPT; ++j)
+#pragma unroll
+      for (int c = 0; c < K; ++c) accr[j][c] = acci[j][c] = 0;
     int lo_w = 0, hi_w = 0, cur_h = -1;
     bool run_touched = false, first_run = true;
     int tile = -1;
     // add register cells [0, CNT) of the window into row cells [cur_h, cur_h + CNT)
     auto flush_cells = [&](auto cnt_tag) {
       constexpr int CNT = decltype(cnt_tag)::value;
-      if (first_run) {  // the previous tile's reduction has finished reading the row
+      if (first_run) {  // the previous tile's reduction has finished reading the rows
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         first_run = false;
         lo_w = hi_w = cur_h;
       }
-      for (int c = hi_w; c < cur_h; ++c) myrow[c] = C{0, 0};
-      for (int c = cur_h + CNT; c < lo_w; ++c) myrow[c] = C{0, 0};
 #pragma unroll
-      for (int t = 0; t < CNT; ++t) {
-        const int c = cur_h + t;
-        C v = C{0, 0};
-        if (c >= lo_w && c < hi_w) v = myrow[c];
-        v.x += accr[t];
-        v.y += acci[t];
-        myrow[c] = v;
+      for (int j = 0; j < RPT; ++j) {
+        if (!owns(j)) continue;
+        C* rw = myrow + j * HS;
+        for (int c = hi_w; c < cur_h; ++c) rw[c] = C{0, 0};
+        for (int c = cur_h + CNT; c < lo_w; ++c) rw[c] = C{0, 0};
+#pragma unroll
+        for (int t = 0; t < CNT; ++t) {
+          const int c = cur_h + t;
+          C v = C{0, 0};
+          if (c >= lo_w && c < hi_w) v = rw[c];
+          v.x += accr[j][t];
+          v.y += acci[j][t];
+          rw[c] = v;
+        }
       }
       lo_w = min(lo_w, cur_h);
       hi_w = max(hi_w, cur_h + CNT);
     };
     // the window moves to start h: by one cell, the leaving cell goes to the
-    // row and the registers shift; otherwise the whole window is flushed
+    // rows and the registers slide; otherwise the whole window is flushed
     auto move_window = [&](int h) {
-      if (run_touched && owner) {
+      if (run_touched && gown) {
         if (h == cur_h + 1 && h <= H2 - K) {
           flush_cells(std::integral_constant<int, 1>{});
 #pragma unroll
-          for (int t = 0; t + 1 < K; ++t) {
-            accr[t] = accr[t + 1];
-            acci[t] = acci[t + 1];
+          for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+            for (int t = 0; t + 1 < K; ++t) {
+              accr[j][t] = accr[j][t + 1];
+              acci[j][t] = acci[j][t + 1];
+            }
+            accr[j][K - 1] = acci[j][K - 1] = 0;
           }
-          accr[K - 1] = acci[K - 1] = 0;
         } else {
           flush_cells(std::integral_constant<int, K>{});
 #pragma unroll
-          for (int t = 0; t < K; ++t) accr[t] = acci[t] = 0;
+          for (int j = 0; j < RPT; ++j)
+#pragma unroll
+            for (int t = 0; t < K; ++t) accr[j][t] = acci[j][t] = 0;
           run_touched = false;
         }
       }
@@ -1424,23 +1446,29 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       auto hits = [&](const int4 r) {
         return (unsigned)r.z <= (unsigned)(H2 - K) && r.x <= wa_hi && r.x + (int)((unsigned)r.w & 0xffu) > wa_lo;
       };
-      // one node: coefficient f * w0[a] * w1[b] against the K last-dim factors
+      // one node: coefficients f * w0[a] * w1[b0 + j] against the K last-dim factors
       auto node1 = [&](const typename P::W* w, const C* fp) {
-        const R s = (R)(w[a] * w[H2 + b]);
+        const typename P::W wa = w[a];
+        R s[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) s[j] = (R)(wa * w[H2 + b0 + j]);
         run_touched = true;
         const C f = *fp;
-        const R cr = f.x * s, ci = f.y * s;
         const C* w2 = reinterpret_cast<const C*>(w + 2 * H2);
         C v[KP];
 #pragma unroll
         for (int p = 0; p < KP; ++p) v[p] = w2[p];
 #pragma unroll
-        for (int p = 0; p < KP; ++p) {
-          accr[2 * p] = fma(cr, (R)v[p].x, accr[2 * p]);
-          acci[2 * p] = fma(ci, (R)v[p].x, acci[2 * p]);
-          if (2 * p + 1 < K) {
-            accr[2 * p + 1] = fma(cr, (R)v[p].y, accr[2 * p + 1]);
-            acci[2 * p + 1] = fma(ci, (R)v[p].y, acci[2 * p + 1]);
+        for (int j = 0; j < RPT; ++j) {
+          const R cr = f.x * s[j], ci = f.y * s[j];
+#pragma unroll
+          for (int p = 0; p < KP; ++p) {
+            accr[j][2 * p] = fma(cr, (R)v[p].x, accr[j][2 * p]);
+            acci[j][2 * p] = fma(ci, (R)v[p].x, acci[j][2 * p]);
+            if (2 * p + 1 < K) {
+              accr[j][2 * p + 1] = fma(cr, (R)v[p].y, accr[j][2 * p + 1]);
+              acci[j][2 * p + 1] = fma(ci, (R)v[p].y, acci[j][2 * p + 1]);
+            }
           }
         }
       };
@@ -1458,31 +1486,51 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }
     }
     if (tile < 0) break;  // end of work
-    if (run_touched && owner) flush_cells(std::integral_constant<int, K>{});
-    if (owner && !first_run && !(g.debug & 1)) {
+    if (run_touched && gown) flush_cells(std::integral_constant<int, K>{});
+    if (gown && !first_run && !(g.debug & 1)) {
       int lo = lo_w, hi = hi_w;
-      if constexpr (sizeof(R) == 4) {  // c64: 16-byte pieces (m, n even: spread_dense_ok)
-        if (lo & 1) myrow[--lo] = C{0, 0};
-        if (hi & 1) myrow[hi++] = C{0, 0};
-      }
-      fence_proxy_async_smem();
       int tc[3];
       tile_of<3>(g, tile, tc);
-      if (g.dense_flush) {
-        int ad = tc[0] * 8 + a - g.m, bd = tc[1] * 8 + b - g.m;
-        ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
-        bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
-        int c0 = tc[2] * 8 - g.m + lo;
-        c0 -= c0 >= g.n[2] ? g.n[2] : 0;
-        bulk_red_row_wrapped<R>(gp, ((int64_t)ad * g.n[1] + bd) * g.n[2], c0, g.n[2], myrow + lo, hi - lo);
-      } else {
-        int64_t row0 = ((int64_t)(tc[0] * 8 + a) * g.np[1] + tc[1] * 8 + b) * g.np[2] + tc[2] * 8 + lo;
-        bulk_red_add<R>(gp + row0, myrow + lo, (unsigned)((hi - lo) * sizeof(C)));
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (!owns(j)) continue;
+        C* rw = myrow + j * HS;
+        if constexpr (sizeof(R) == 4) {  // c64: 16-byte pieces (m, n even: spread_dense_ok)
+          if (lo & 1) rw[lo - 1] = C{0, 0};
+          if (hi & 1) rw[hi] = C{0, 0};
+        }
+      }
+      if constexpr (sizeof(R) == 4) {
+        lo -= lo & 1;
+        hi += hi & 1;
+      }
+      fence_proxy_async_smem();
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (!owns(j)) continue;
+        const int b = b0 + j;
+        C* rw = myrow + j * HS;
+        if (g.dense_flush) {
+          int ad = tc[0] * 8 + a - g.m, bd = tc[1] * 8 + b - g.m;
+          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+          bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
+          int c0 = tc[2] * 8 - g.m + lo;
+          c0 -= c0 >= g.n[2] ? g.n[2] : 0;
+          bulk_red_row_wrapped<R>(gp, ((int64_t)ad * g.n[1] + bd) * g.n[2], c0, g.n[2], rw + lo, hi - lo);
+        } else {
+          int64_t row0 = ((int64_t)(tc[0] * 8 + a) * g.np[1] + tc[1] * 8 + b) * g.np[2] + tc[2] * 8 + lo;
+          bulk_red_add<R>(gp + row0, rw + lo, (unsigned)((hi - lo) * sizeof(C)));
+        }
       }
       asm volatile("cp.async.bulk.commit_group;\n" ::);
     }
   }
   } else {
+  const int row = threadIdx.x;
+  const bool owner = row < P::ROWS;  // non-owners accumulate garbage that is never flushed
+  const int a = owner ? row / H2 : 0, b = owner ? row % H2 : 0;
+  const int wa_lo = min((int)(threadIdx.x & ~31u), P::ROWS - 1) / H2;
+  const int wa_hi = min((int)(threadIdx.x | 31u), P::ROWS - 1) / H2;
   for (;;) {  // tiles of this CTA
     R accr[H2], acci[H2];
 #pragma unroll
