@@ -406,9 +406,12 @@ static void nodes_to_device(Plan* p, cudaStream_t s) {
   p->geom.rec = p->rec;
 }
 
+// New nodes invalidate the tables; the PRE_PSI allocation itself is kept
+// (precompute rebuilds it in place when the size matches): freeing and
+// re-allocating tens of GiB cost ~0.2 s per set_nodes at C5.
 static void invalidate_tables(Plan* p) {
   p->ready = false;
-  if (p->psi) { cudaFree(p->psi); p->psi = nullptr; }
+  p->geom.psi = nullptr;
 }
 
 void plan_set_nodes_host(Plan* p, const double* x, int64_t len) {

@@ -9,7 +9,7 @@ path: zero-copy, ordered on the current torch stream, returns a tensor).
 
 import ctypes
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -82,8 +82,23 @@ class PrecomputeTables:
     psi: np.ndarray = None
     psi_on_device: bool = False
     lut_on_device: bool = False
-    node_order: np.ndarray = None
     window_evals: int = 0
+    # node_order (plan.py:120, :296) is materialised on first access: at C5
+    # it is a 512 MiB int64 host array from a device lexsort, which the
+    # transforms never need
+    _order_source: object = field(default=None, repr=False, compare=False)
+    _node_order: np.ndarray = field(default=None, repr=False, compare=False)
+
+    @property
+    def node_order(self):
+        if self._node_order is None and self._order_source is not None:
+            self._node_order = self._order_source()
+        return self._node_order
+
+    @node_order.setter
+    def node_order(self, value):
+        self._node_order = value
+        self._order_source = None
 
 
 def _is_torch(a):
@@ -286,7 +301,7 @@ class Plan:
         if self.f1 & PRE_LIN_PSI:
             evals += self.d * (LUT_SIZE + 1)
         t.window_evals = evals
-        t.node_order = self.node_order
+        t._order_source = lambda: self.node_order
         return t
 
     def phi_hut(self, i):

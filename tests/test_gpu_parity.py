@@ -293,6 +293,9 @@ def test_node_order_matches_lexsort(oracle):
         c = case(name)
         p = make_plan(c)
         assert np.array_equal(p.node_order, c["order"])
+        # the tables precompute returns (plan.py:296) carry the same order,
+        # materialised on first access
+        assert np.array_equal(p.precompute().node_order, c["order"])
 
 
 def test_window_eval_counter():
