@@ -212,7 +212,12 @@ static void choose_tiles(Plan* p) {
   while (g.nb_spread > 4 && spread_smem_nb(g, (int)eb, g.nb_spread) > 220 * KB) g.nb_spread /= 2;
   g.nt_interp = interp_smem(g, (int)eb, 256) > 110 * KB ? 512 : 256;
   g.nt_interp = env_int("NFFTK_INTERP_THREADS", g.nt_interp);
-  p->maxsub = env_int("NFFTK_MAXSUB", 1024);
+  // nodes per subproblem (one CTA): at most 1024, and small enough that a
+  // small plan still spreads over the SMs (C1: 4 tiles of 1024 nodes would
+  // run on 4 CTAs)
+  int ms = 1024;
+  while (ms > 32 && (int64_t)ms * 4 * 148 > p->M) ms /= 2;
+  p->maxsub = env_int("NFFTK_MAXSUB", ms);
   g.debug = env_int("NFFTK_DEBUG", 0);
 }
 
