@@ -122,6 +122,14 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU legs
+def host_cores():
+    """Host threads the CPU legs may use (torchrun sets OMP_NUM_THREADS=1)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_oracle_rate(w, seconds, seed_offset=0):
     """Time the CPU oracle port (trafo + adjoint) on a bounded node sample.
 
@@ -131,6 +139,7 @@ def cpu_oracle_rate(w, seconds, seed_offset=0):
     """
     from oracle import oracle as O
 
+    O.set_threads(host_cores())
     threads = O.max_threads()
     M = w.M
     base = wl.scaled(w, M)
@@ -170,6 +179,7 @@ def run_reference(args):
     w = wl.CONFIGS[args.config]
     from oracle import oracle as O
 
+    O.set_threads(host_cores())
     threads = O.max_threads()
     x = wl.nodes(w)
     fh = wl.fhat(w)
@@ -212,10 +222,18 @@ def main():
     from paper_1810_09891_b200.distributed import DistributedPlan
 
     rank, world, local = env_rank()
+    # NFFTK_DIST_BACKEND=gloo: functional check of the N>1 orchestration on a
+    # one-GPU box (ranks share the device; not a measurement)
+    backend = os.environ.get("NFFTK_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     w = wl.CONFIGS[args.config]
     cdt = torch.complex64 if args.precision == "single" else torch.complex128
     s_elem = 8 if args.precision == "single" else 16

@@ -593,3 +593,13 @@ int oracle_max_threads(void) {
     return 1;
 #endif
 }
+
+/* Thread count for the following parallel regions (torchrun exports
+ * OMP_NUM_THREADS=1 to every rank; the CPU baseline wants the host's cores). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}

@@ -62,6 +62,8 @@ def lib():
         L.oracle_window_b.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_window_b.restype = ctypes.c_double
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_threads.restype = None
         _lib = L
     return _lib
 
@@ -193,6 +195,11 @@ def window_b(kind, N_i, n_i, m):
 
 def max_threads():
     return lib().oracle_max_threads()
+
+
+def set_threads(n):
+    """OpenMP threads for the oracle's parallel loops (0 / negative: unchanged)."""
+    lib().oracle_set_threads(int(n))
 
 
 def error_e2(ref, approx):
