@@ -20,6 +20,11 @@ static unsigned long long g_launches = 0;  // kernels launched by this library
 unsigned long long launch_count() { return g_launches; }
 void count_launch() { ++g_launches; }
 
+// cells per segment when a line of len cells is cut into nseg warp-sized pieces
+__host__ __device__ inline int seg_width(int len, int nseg) {
+  return nseg <= 1 ? len : ((len + nseg - 1) / nseg + 31) / 32 * 32;
+}
+
 static inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148LL * 64) {
   int64_t b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -375,13 +380,17 @@ struct DeconvGeom {
 template <typename R>
 __global__ void __launch_bounds__(256) k_deconv_pad(const cplx_t<R>* __restrict__ fhat,
                                                     cplx_t<R>* __restrict__ grid, DeconvGeom q,
-                                                    int64_t lines) {
+                                                    int64_t lines, int nseg) {
   using C = cplx_t<R>;
   const int dl = q.d - 1;
   const int nl = q.n[dl], Nl = q.N[dl], h = Nl / 2;
   const int lane = threadIdx.x & 31;
   const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t line = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+  const int segw = seg_width(nl, nseg);
+  for (int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < lines * nseg;
+       item += wstride) {
+    const int64_t line = item / nseg;
+    const int s0 = (int)(item - line * nseg) * segw, s1 = min(nl, s0 + segw);
     bool inside = true;
     int64_t fl = 0, rem = line;
     double fac = q.inv_gs;
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(256) k_deconv_pad(const cplx_t<R>* __restrict_
     }
     C* out = grid + line * nl;
     const C* in = fhat + fl * Nl;
-    for (int sl = lane; sl < nl; sl += 32) {
+    for (int sl = s0 + lane; sl < s1; sl += 32) {
       C v;
       v.x = 0;
       v.y = 0;
@@ -415,13 +424,17 @@ __global__ void __launch_bounds__(256) k_deconv_pad(const cplx_t<R>* __restrict_
 template <typename R>
 __global__ void __launch_bounds__(256) k_pack_deconv(const cplx_t<R>* __restrict__ grid,
                                                      cplx_t<R>* __restrict__ fhat, DeconvGeom q,
-                                                     int64_t lines) {
+                                                     int64_t lines, int nseg) {
   using C = cplx_t<R>;
   const int dl = q.d - 1;
   const int nl = q.n[dl], Nl = q.N[dl];
   const int lane = threadIdx.x & 31;
   const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t line = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+  const int segw = seg_width(Nl, nseg);
+  for (int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < lines * nseg;
+       item += wstride) {
+    const int64_t line = item / nseg;
+    const int s0 = (int)(item - line * nseg) * segw, s1 = min(Nl, s0 + segw);
     int64_t gl = 0, rem = line;
     double fac = q.inv_gs;
     int kidx[MAX_D];
@@ -433,7 +446,7 @@ __global__ void __launch_bounds__(256) k_pack_deconv(const cplx_t<R>* __restrict
     }
     const C* in = grid + gl * nl;
     C* out = fhat + line * Nl;
-    for (int kl = lane; kl < Nl; kl += 32) {
+    for (int kl = s0 + lane; kl < s1; kl += 32) {
       int k = kl - Nl / 2;
       C a = in[k < 0 ? k + nl : k];
       double f = fac * q.icol[dl][kl];
@@ -450,11 +463,22 @@ static unsigned line_blocks(int64_t lines) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148LL * 16));
 }
 
+// Segments per line for the warp-per-line kernels: few, long lines (d = 1:
+// one line) are cut into 32-cell multiples so a small grid still spreads
+// over the SMs (C1: one warp walked all 2048 cells of the only line).
+static int line_segments(int64_t lines, int len) {
+  const int64_t target = 148LL * 64;  // warps
+  int64_t seg = std::max<int64_t>(1, target / std::max<int64_t>(1, lines));
+  return (int)std::min<int64_t>(seg, (len + 31) / 32);
+}
+
 template <typename R>
 void launch_deconv_pad(const void* fhat, void* grid, const DeconvGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.n[i];
-  k_deconv_pad<R><<<line_blocks(lines), 256, 0, s>>>((const cplx_t<R>*)fhat, (cplx_t<R>*)grid, q, lines);
+  const int nseg = line_segments(lines, q.n[q.d - 1]);
+  k_deconv_pad<R><<<line_blocks(lines * nseg), 256, 0, s>>>((const cplx_t<R>*)fhat, (cplx_t<R>*)grid, q,
+                                                            lines, nseg);
   count_launch();
 }
 
@@ -462,7 +486,9 @@ template <typename R>
 void launch_pack_deconv(const void* grid, void* fhat, const DeconvGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.N[i];
-  k_pack_deconv<R><<<line_blocks(lines), 256, 0, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)fhat, q, lines);
+  const int nseg = line_segments(lines, q.N[q.d - 1]);
+  k_pack_deconv<R><<<line_blocks(lines * nseg), 256, 0, s>>>((const cplx_t<R>*)grid, (cplx_t<R>*)fhat, q,
+                                                             lines, nseg);
   count_launch();
 }
 
@@ -552,31 +578,37 @@ __device__ __forceinline__ int wrap_slot(int p, int m, int n) {
 
 template <typename C>
 __global__ void __launch_bounds__(256) k_pad(const C* __restrict__ g0, C* __restrict__ gp, PadGeom q,
-                                             int lines) {
+                                             int lines, int nseg) {
   const int dl = q.d - 1;
   const int nl = q.n[dl], npl = q.np[dl];
   const int lane = threadIdx.x & 31;
   const int wstride = (gridDim.x * blockDim.x) >> 5;
-  for (int line = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+  const int segw = seg_width(npl, nseg);
+  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < lines * nseg; item += wstride) {
+    const int line = item / nseg;
+    const int s0 = (item - line * nseg) * segw, s1 = min(npl, s0 + segw);
     int src = 0, rem = line;
     int lead[MAX_D];
     for (int i = dl - 1; i >= 0; --i) { lead[i] = rem % q.np[i]; rem /= q.np[i]; }
     for (int i = 0; i < dl; ++i) src = src * q.n[i] + wrap_slot(lead[i], q.m, q.n[i]);
     const C* in = g0 + (int64_t)src * nl;
     C* out = gp + (int64_t)line * npl;
-    for (int p = lane; p < npl; p += 32) out[p] = in[wrap_slot(p, q.m, nl)];
+    for (int p = s0 + lane; p < s1; p += 32) out[p] = in[wrap_slot(p, q.m, nl)];
   }
 }
 
 // padded -> dense (after the spread): each dense cell sums its images
 template <typename C>
 __global__ void __launch_bounds__(256) k_fold(const C* __restrict__ gp, C* __restrict__ g0, PadGeom q,
-                                              int lines) {
+                                              int lines, int nseg) {
   const int dl = q.d - 1;
   const int nl = q.n[dl], npl = q.np[dl];
   const int lane = threadIdx.x & 31;
   const int wstride = (gridDim.x * blockDim.x) >> 5;
-  for (int line = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; line < lines; line += wstride) {
+  const int segw = seg_width(nl, nseg);
+  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < lines * nseg; item += wstride) {
+    const int line = item / nseg;
+    const int s0 = (item - line * nseg) * segw, s1 = min(nl, s0 + segw);
     int rem = line;
     int c[MAX_D];
     for (int i = dl - 1; i >= 0; --i) { c[i] = rem % q.n[i]; rem /= q.n[i]; }
@@ -598,7 +630,7 @@ __global__ void __launch_bounds__(256) k_fold(const C* __restrict__ gp, C* __res
       np_lines = nt;
     }
     C* out = g0 + (int64_t)line * nl;
-    for (int s2 = lane; s2 < nl; s2 += 32) {
+    for (int s2 = s0 + lane; s2 < s1; s2 += 32) {
       double re = 0, im = 0;
       const int p0 = s2 + q.m;
       const bool lo_img = p0 - nl >= 0, hi_img = p0 + nl < npl;
@@ -629,16 +661,20 @@ __global__ void __launch_bounds__(256) k_fold(const C* __restrict__ gp, C* __res
 void launch_pad(bool single, const void* g0, void* gp, const PadGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.np[i];
-  if (single) k_pad<float2><<<line_blocks(lines), 256, 0, s>>>((const float2*)g0, (float2*)gp, q, (int)lines);
-  else k_pad<double2><<<line_blocks(lines), 256, 0, s>>>((const double2*)g0, (double2*)gp, q, (int)lines);
+  const int nseg = line_segments(lines, q.np[q.d - 1]);
+  const unsigned nb = line_blocks(lines * nseg);
+  if (single) k_pad<float2><<<nb, 256, 0, s>>>((const float2*)g0, (float2*)gp, q, (int)lines, nseg);
+  else k_pad<double2><<<nb, 256, 0, s>>>((const double2*)g0, (double2*)gp, q, (int)lines, nseg);
   count_launch();
 }
 
 void launch_fold(bool single, const void* gp, void* g0, const PadGeom& q, cudaStream_t s) {
   int64_t lines = 1;
   for (int i = 0; i < q.d - 1; ++i) lines *= q.n[i];
-  if (single) k_fold<float2><<<line_blocks(lines), 256, 0, s>>>((const float2*)gp, (float2*)g0, q, (int)lines);
-  else k_fold<double2><<<line_blocks(lines), 256, 0, s>>>((const double2*)gp, (double2*)g0, q, (int)lines);
+  const int nseg = line_segments(lines, q.n[q.d - 1]);
+  const unsigned nb = line_blocks(lines * nseg);
+  if (single) k_fold<float2><<<nb, 256, 0, s>>>((const float2*)gp, (float2*)g0, q, (int)lines, nseg);
+  else k_fold<double2><<<nb, 256, 0, s>>>((const double2*)gp, (double2*)g0, q, (int)lines, nseg);
   count_launch();
 }
 }  // namespace nfftk
