@@ -136,3 +136,38 @@ def test_pin_kb_edge_limit(oracle):
     """Reference test_window.py:44-48: phi(m/n) = b/pi exactly on the u == 0 branch."""
     b = oracle.window_b(0, 16, 32, 4)
     assert oracle.window_factor(0, 4 / 32, 32, 4, b) == b / np.pi
+
+
+# --- the reference's own property pins, restated (test_fft.py:31-86,
+# test_window.py:147-186): the oracle's FFT against numpy, and the closed-form
+# phi_hat against quadrature of the window it transforms.
+@pytest.mark.parametrize("shape", [(16,), (514,), (8, 12), (6, 10, 4), (32, 34)])
+@pytest.mark.parametrize("sign", [-1, +1])
+def test_oracle_fft_matches_numpy(oracle, shape, sign):
+    """Unnormalised separable FFT, both signs; radix-2 and Bluestein lengths
+    (fft.py:63-139)."""
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    ref = np.fft.fftn(a) if sign < 0 else np.fft.ifftn(a) * a.size
+    out = oracle.fft_nd(a, sign)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-13
+
+
+@pytest.mark.parametrize("kind,N,n,m", [("kaiserbessel", 16, 32, 4), ("kaiserbessel", 64, 128, 6),
+                                        ("kaiserbessel", 32, 48, 3), ("gaussian", 16, 32, 4),
+                                        ("gaussian", 64, 128, 6)])
+def test_oracle_phi_hat_matches_quadrature(oracle, kind, N, n, m):
+    """phi_hat(k) (window.py:142-164) is the Fourier integral of the window
+    (the reference gates the closed forms at 1e-8 against its quadrature
+    oracle).  Kaiser-Bessel is integrated over its support |t| <= m/n only:
+    the window's sin-branch tail beyond it carries ~1e-9 of the integral."""
+    from scipy.integrate import quad
+
+    code = 1 if kind == "gaussian" else 0
+    b = oracle.window_b(code, N, n, m)
+    lim = m / n if code == 0 else 40.0 * np.sqrt(b) / n
+    for k in (0, 1, N // 4, N // 2 - 1, -N // 2):
+        val, _ = quad(lambda t: oracle.window_factor(code, t, n, m, b) * np.cos(2 * np.pi * k * t),
+                      -lim, lim, limit=400, epsabs=0, epsrel=1e-12)
+        ph = oracle.phi_hat(code, k, n, m, b)
+        assert abs(val - ph) <= 1e-8 * abs(ph), (k, val, ph)
