@@ -128,7 +128,28 @@ struct Geom {
   int debug;              // NFFTK_DEBUG bits (experiments only; 0 in production)
   int dense_flush;        // pipelined c128 spread reduces into the dense grid (periodic wrap per row), no fold
   int psi_f32;            // PRE_PSI rows stored as fp32 (c64 plans on the pipelined geometries); psi then points at floats
+  unsigned* sched;        // plan-owned ticket counters for persistent kernels (SCHED_* slots; null: static order)
 };
+
+// Dynamic subproblem order for the persistent gridding kernels: CTA b starts at
+// subproblem b, then draws tickets gridDim.x + t from a counter, so CTAs that
+// drew light tiles take more (clustered nodes: C4).  Each CTA draws exactly
+// one failing ticket, so the counter ends at nsubs; the last CTA to finish
+// resets it for the next launch on the stream.
+enum { SCHED_SPREAD3 = 0, SCHED_SPREAD2 = 2, SCHED_INTERP = 4, SCHED_SLOTS = 8 };
+__device__ __forceinline__ int next_sub(const Geom& g, int slot, int cur) {
+  if (!g.sched) return cur + (int)gridDim.x;
+  return (int)gridDim.x + (int)atomicAdd(g.sched + slot, 1u);
+}
+__device__ __forceinline__ void sched_done(const Geom& g, int slot) {
+  if (!g.sched) return;
+  __threadfence();
+  if (atomicAdd(g.sched + slot + 1, 1u) == gridDim.x - 1) {
+    g.sched[slot] = 0;
+    g.sched[slot + 1] = 0;
+    __threadfence();
+  }
+}
 
 // -------------------------------------------------------- device window
 // window.py:56-72.  Explicit _rn intrinsics keep the reference's rounding

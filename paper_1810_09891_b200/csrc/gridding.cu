@@ -606,7 +606,7 @@ struct IPipeCfg {
   static constexpr size_t SB = W_BYTES + R_BYTES + al(4 * (size_t)(NB + 4));
   static constexpr size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
   static constexpr size_t HALO = al128((size_t)ROWS * HS * ELEM);  // TMA tensor destinations: 128 B
-  static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMetaI) * s + 32 + 16); }
+  static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMetaI) * s + 64 + 16); }
   static constexpr size_t halo_off(int s) { return al128(s * SB + ctl_bytes(s)); }
   static constexpr size_t LIMIT = 224 * 1024;
   // prefer double-buffered halos (next halo loads under the current tile),
@@ -638,7 +638,8 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
   unsigned long long* empty = full + S;
   unsigned long long* hbar = empty + S;  // NH halo barriers
   StageMetaI* meta = reinterpret_cast<StageMetaI*>(hbar + 2);
-  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, k
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, k, drawn, seq
+  int* subq = pst + 6;                           // the CTA's subproblem sequence (ring of 8)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane % TEAM, sub = lane / TEAM;
   const unsigned halo_tx = (unsigned)(P::ROWS * HS * sizeof(C));
@@ -674,6 +675,9 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     for (int i = 0; i < NH; ++i) mbar_init(hbar + i, 1);
     pst[0] = blockIdx.x;
     pst[3] = 0;
+    pst[4] = 1;  // subproblems drawn (the first is blockIdx.x)
+    pst[5] = 0;  // producer's position in the sequence
+    subq[0] = blockIdx.x;
     if (blockIdx.x < nsubs) {
       const int4 sp = subs[blockIdx.x];
       pst[1] = sp.y;
@@ -681,6 +685,16 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     }
   }
   __syncthreads();
+  // j-th subproblem of this CTA (thread 0 only): producer and halo issue walk
+  // the same sequence; dynamic tickets (next_sub), no draw past the end
+  auto sub_at = [&](int j) {
+    while (pst[4] <= j) {
+      const int prev = subq[(pst[4] - 1) & 7];
+      subq[pst[4] & 7] = prev >= nsubs ? prev : next_sub(g, SCHED_INTERP, prev);
+      ++pst[4];
+    }
+    return subq[j & 7];
+  };
   auto produce = [&]() {
     const int pk = pst[3];
     const int slot = pk % S;
@@ -708,7 +722,7 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {
-      const int s = pst[0] + gridDim.x;
+      const int s = sub_at(++pst[5]);
       pst[0] = s;
       if (s < nsubs) {
         const int4 sp = subs[s];
@@ -722,17 +736,21 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     if (NH == 2 && (int)blockIdx.x < nsubs) issue_halo(blockIdx.x, 0);
   }
   int k = 0;
-  int it = 0;
-  for (int s = blockIdx.x; s < nsubs; s += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {  // subproblems of this CTA, in sub_at order
     const int buf = NH == 2 ? (it & 1) : 0;
     __syncthreads();  // every warp is done with the halo buffer about to be refilled
     if (threadIdx.x == 0) {
       if constexpr (NH == 1) {
-        issue_halo(s, 0);
+        const int s = sub_at(it);
+        if (s < nsubs) issue_halo(s, 0);
       } else {
-        if (s + (int)gridDim.x < nsubs) issue_halo(s + gridDim.x, buf ^ 1);
+        const int s = sub_at(it + 1);
+        if (s < nsubs) issue_halo(s, buf ^ 1);
       }
     }
+    // the ring says whether a subproblem follows (end marker: no halo was issued)
+    mbar_wait(full + k % S, (k / S) & 1);
+    if (meta[k % S].nb < 0) break;
     mbar_wait(hbar + buf, (NH == 2 ? (it >> 1) : it) & 1);
     const C* halo = reinterpret_cast<const C*>(smem + P::HALO_OFF + buf * P::HALO);
     for (;; ++k) {  // batches of the subproblem
@@ -808,6 +826,18 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
       }
     }
   }
+  if (threadIdx.x == 0) sched_done(g, SCHED_INTERP);
+}
+
+// Dynamic tickets pay where a CTA walks many subproblems of uneven weight
+// (clustered C4: spread 2.90 -> 2.35 ms, interp 2.59 -> 2.41); with a
+// handful per CTA (C2: 1.5 per spread CTA, 12 per interp CTA) the ticket
+// latency on the producer's and halo issue's path costs more than the
+// balance gains (C2 step 0.120 -> 0.126 ms with dynamic interp tickets).
+static Geom sched_geom(const Geom& g, int nsubs, int grid, int per_cta = 4) {
+  Geom q = g;
+  if ((int64_t)nsubs < (int64_t)per_cta * grid) q.sched = nullptr;
+  return q;
 }
 
 // Geometries the pipelined kernels (spread and interp) both cover; for d = 3
@@ -1334,7 +1364,7 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {
-      const int s = pst[0] + gridDim.x;
+      const int s = next_sub(g, SCHED_SPREAD3, pst[0]);
       pst[0] = s;
       if (s < nsubs) {
         const int4 sp = subs[s];
@@ -1652,6 +1682,7 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     }
   }
   }  // RUNACC
+  if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD3);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
@@ -1745,7 +1776,7 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {
-      const int s = pst[0] + gridDim.x;
+      const int s = next_sub(g, SCHED_SPREAD2, pst[0]);
       pst[0] = s;
       if (s < nsubs) {
         const int4 sp = subs[s];
@@ -1865,6 +1896,7 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       asm volatile("cp.async.bulk.commit_group;\n" ::);
     }
   }
+  if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD2);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
@@ -1946,7 +1978,8 @@ static void interp_go(const CUtensorMap* tm, const void* gp, void* f, void*, con
       int per_sm = 0;
       NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
       int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
-      kern<<<grid, P::THREADS, P::SMEM, s>>>(*tm, (cplx_t<R>*)f, g.psi, g.rec, perm, subs, nsubs, g);
+      kern<<<grid, P::THREADS, P::SMEM, s>>>(*tm, (cplx_t<R>*)f, g.psi, g.rec, perm, subs, nsubs,
+                                           sched_geom(g, nsubs, grid, 16));
       count_launch();
       return;
     }
@@ -1993,7 +2026,7 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
         NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
         int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
         kern<<<grid, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs,
-                                               nsubs, g);
+                                               nsubs, sched_geom(g, nsubs, grid));
         count_launch();
         return;
       }
@@ -2033,7 +2066,8 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
       int per_sm = 0;
       NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, P::SMEM));
       int grid = std::max(1, std::min(nsubs, sms2 * std::max(1, per_sm)));
-      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs, nsubs, g);
+      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs, nsubs,
+                                     sched_geom(g, nsubs, grid));
       count_launch();
       return;
     }

@@ -122,6 +122,7 @@ Plan::~Plan() {
   cudaFree(cols);
   if (!grid_external) cudaFree(grid);
   cudaFree(gp);
+  cudaFree(sched);
   cudaFree(fhat_dev);
   cudaFree(f_dev);
   cudaFree(f_sorted);
@@ -501,6 +502,11 @@ static void build_tensor_map(Plan* p) {
 
 static void ensure_grid(Plan* p) {
   if (!p->grid) NFFTK_CUDA(cudaMalloc(&p->grid, p->elem_bytes() * p->grid_size));
+  if (!p->sched) {
+    NFFTK_CUDA(cudaMalloc(&p->sched, sizeof(unsigned) * SCHED_SLOTS));
+    NFFTK_CUDA(cudaMemset(p->sched, 0, sizeof(unsigned) * SCHED_SLOTS));
+  }
+  p->geom.sched = getenv("NFFTK_STATIC_SCHED") ? nullptr : p->sched;
   if (!p->gp) {
     size_t cells = 1;
     for (int i = 0; i < p->d; ++i) cells *= (size_t)p->geom.np[i];

@@ -61,6 +61,7 @@ struct Plan {
   void* grid = nullptr;              // dense n-grid (cuFFT, deconvolution)
   bool grid_external = false;
   void* gp = nullptr;                // ghost-padded grid (gridding kernels)
+  unsigned* sched = nullptr;         // ticket counters of the persistent spread kernels (SCHED_SLOTS)
   size_t gp_bytes = 0;
   PadGeom pq{};
   alignas(64) unsigned char tmap[128];  // CUtensorMap of gp (halo boxes)
