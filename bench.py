@@ -467,6 +467,15 @@ def kernel_names(w, tile, psi):
     return {"interp": "k_interp", "spread": "k_spread_rr" if rr else "k_spread"}
 
 
+# What bounds each gridding kernel (ncu summaries in
+# profiles/): neither is HBM-bound at these cutoffs; "hbm" is the contract's
+# roofline, reported with the compulsory bytes.
+BINDING = {
+    "interp": "shared-memory wavefronts (one 16-byte halo cell per node-cell)",
+    "spread": "FP64 FMA issue and per-node latency of the register-resident halo walk",
+}
+
+
 def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None):
     """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
     M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
@@ -488,6 +497,7 @@ def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None):
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
             "traffic": ncu_traffic(w.name, kname), "algorithmic_bytes_per_launch": traffic_alg,
             "avg_launch_ms": per, "peak_source": peaks["source"],
+            "binding_resource": BINDING.get(ph, ""),
             "fma": {"achieved_tflops": tflops, "peak_tflops": fma_tflops,
                     "frac": tflops / fma_tflops if fma_tflops else None,
                     "flops_per_launch": flops,
