@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -274,6 +275,21 @@ static int bits_for(unsigned long long v) {
   return b < 1 ? 1 : b;
 }
 
+// weight class of a subproblem, 0 = heaviest (count near maxsub)
+__global__ void k_sub_keys(const int4* __restrict__ subs, int total, int maxsub,
+                           uint32_t* __restrict__ keys, int* __restrict__ vals) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  keys[i] = (uint32_t)(((int64_t)(maxsub - subs[i].z) * 8) / (maxsub + 1));
+  vals[i] = i;
+}
+
+__global__ void k_gather_subs(const int4* __restrict__ subs, const int* __restrict__ order, int total,
+                              int4* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) out[i] = subs[order[i]];
+}
+
 void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int ntiles,
                   int* perm, double* xs, int* tile_count, int* tile_start, int4** subs,
                   int* nsubs, cudaStream_t s) {
@@ -319,6 +335,34 @@ void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int
                                                    maxsub, *subs);
   count_launch();
   *nsubs = total;
+  // heaviest subproblems first, in 8 weight classes (ties keep tile order):
+  // with clustered nodes the last subproblems a persistent CTA draws are
+  // then light, which shortens the tail; evenly filled tiles all land in one
+  // class and keep their order
+  if (total > 1 && !getenv("NFFTK_NO_LPT")) {
+    uint32_t* sk = nullptr;
+    int* sv = nullptr;
+    int4* sorted = nullptr;
+    NFFTK_CUDA(cudaMallocAsync(&sk, sizeof(uint32_t) * total * 2, s));
+    NFFTK_CUDA(cudaMallocAsync(&sv, sizeof(int) * total * 2, s));
+    NFFTK_CUDA(cudaMalloc(&sorted, sizeof(int4) * total));
+    k_sub_keys<<<(total + 255) / 256, 256, 0, s>>>(*subs, total, maxsub, sk, sv);
+    count_launch();
+    size_t lb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, lb, sk, sk + total, sv, sv + total, total, 0, 3, s);
+    void* ltmp = nullptr;
+    NFFTK_CUDA(cudaMallocAsync(&ltmp, lb, s));
+    NFFTK_CUDA(cub::DeviceRadixSort::SortPairs(ltmp, lb, sk, sk + total, sv, sv + total, total, 0, 3, s));
+    count_launch();
+    k_gather_subs<<<(total + 255) / 256, 256, 0, s>>>(*subs, sv + total, total, sorted);
+    count_launch();
+    NFFTK_CUDA(cudaFreeAsync(ltmp, s));
+    NFFTK_CUDA(cudaFreeAsync(sv, s));
+    NFFTK_CUDA(cudaFreeAsync(sk, s));
+    NFFTK_CUDA(cudaStreamSynchronize(s));
+    NFFTK_CUDA(cudaFree(*subs));
+    *subs = sorted;
+  }
   NFFTK_CUDA(cudaFreeAsync(tmp, s));
   NFFTK_CUDA(cudaFreeAsync(nsub, s));
   NFFTK_CUDA(cudaFreeAsync(vals, s));
