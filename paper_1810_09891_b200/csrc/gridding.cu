@@ -283,18 +283,61 @@ __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, 
       R w1r[WF];
 #pragma unroll
       for (int t = 0; t < WF; ++t) w1r[t] = (R)wl[t];
-      for (int t0 = tl; t0 < WF; t0 += TEAM) {
-        const C* row = halo + (q[0] + t0) * HS + q[1];
+      if constexpr (WF == 12 && TEAM == 8 && sizeof(R) == 8) {
+        // 12 rows on 8 lanes: rows 0..7 whole, then rows 8..11 split between
+        // lane pairs.  With an odd row stride the 4 rows a phase-2 quarter
+        // warp reads start in the bank-group set D = {0, 2, 5, 7} (+ shift);
+        // the two halves read columns u and u + 4 -- D and D + 4 are
+        // disjoint, so those loads are conflict-free -- then columns 8..9 /
+        // 10..11.  20 instead of 24 wavefronts per node (half the lanes
+        // idled through rows 8..11 before).
+        {
+          const C* row = halo + (q[0] + tl) * HS + q[1];
+          R sre = 0, sim = 0;
+#pragma unroll
+          for (int t = 0; t < WF; ++t) {
+            C v = row[t];
+            sre = fma(w1r[t], v.x, sre);
+            sim = fma(w1r[t], v.y, sim);
+          }
+          R f0 = (R)w0[o0 + tl];
+          are = fma(f0, sre, are);
+          aim = fma(f0, sim, aim);
+        }
+        const int j = tl & 3, h = tl >> 2;
+        const C* row = halo + (q[0] + 8 + j) * HS + q[1];
         R sre = 0, sim = 0;
 #pragma unroll
-        for (int t = 0; t < WF; ++t) {
-          C v = row[t];
-          sre = fma(w1r[t], v.x, sre);
-          sim = fma(w1r[t], v.y, sim);
+        for (int u = 0; u < 4; ++u) {
+          C v = row[u + 4 * h];
+          const R w = h ? w1r[u + 4] : w1r[u];
+          sre = fma(w, v.x, sre);
+          sim = fma(w, v.y, sim);
         }
-        R f0 = (R)w0[o0 + t0];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          C v = row[8 + 2 * h + u];
+          const R w = h ? w1r[10 + u] : w1r[8 + u];
+          sre = fma(w, v.x, sre);
+          sim = fma(w, v.y, sim);
+        }
+        R f0 = (R)w0[o0 + 8 + j];
         are = fma(f0, sre, are);
         aim = fma(f0, sim, aim);
+      } else {
+        for (int t0 = tl; t0 < WF; t0 += TEAM) {
+          const C* row = halo + (q[0] + t0) * HS + q[1];
+          R sre = 0, sim = 0;
+#pragma unroll
+          for (int t = 0; t < WF; ++t) {
+            C v = row[t];
+            sre = fma(w1r[t], v.x, sre);
+            sim = fma(w1r[t], v.y, sim);
+          }
+          R f0 = (R)w0[o0 + t0];
+          are = fma(f0, sre, are);
+          aim = fma(f0, sim, aim);
+        }
       }
     } else {
       R w2r[WF];
