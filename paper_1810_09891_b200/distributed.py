@@ -57,15 +57,32 @@ class DistributedNfft:
         """Samples at this rank's nodes (no communication)."""
         return self.engine.trafo(fhat)
 
-    def adjoint(self, f_local, out=None):
-        """Full coefficient vector, identical on every rank."""
+    def adjoint(self, f_local, out=None, async_op=False):
+        """Full coefficient vector, identical on every rank.
+
+        ``async_op=True`` (coefficient reduction) returns ``(fhat, work)``:
+        the all-reduce is in flight and ``work.wait()`` orders it before
+        later work on the current stream, so independent work -- e.g. the
+        trafo of a trafo + adjoint step -- overlaps the exchange (on NCCL the
+        collective runs on its own stream)."""
         grid = self.engine.spread(f_local)
         if self.reduce == "grid" and self.world > 1:
             dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=self.group)
         fhat = self.engine.finish(grid) if out is None else self.engine.finish(grid, out=out)
+        work = None
         if self.reduce == "fhat" and self.world > 1:
-            dist.all_reduce(torch.view_as_real(fhat), op=dist.ReduceOp.SUM, group=self.group)
+            work = dist.all_reduce(torch.view_as_real(fhat), op=dist.ReduceOp.SUM, group=self.group,
+                                   async_op=async_op)
+        if async_op:
+            return fhat, (work if work is not None else _Done())
         return fhat
+
+
+class _Done:
+    """Completed-work stand-in (one rank, or the grid reduction already done)."""
+
+    def wait(self):
+        return True
 
 
 class GpuEngine:

@@ -56,8 +56,10 @@ def _worker(rank, world, port, case, reduce, q):
         f = rng.standard_normal(M) + 1j * rng.standard_normal(M)
         lo, hi = shard_bounds(M, world, rank)
         eng = DistributedNfft(OracleEngine(N, n, m, x[lo:hi]), reduce=reduce)
+        # adjoint first with the exchange in flight, the trafo overlapping it
+        a, work = eng.adjoint(torch.from_numpy(f[lo:hi]), async_op=True)
         f_loc = eng.trafo(torch.from_numpy(fh))
-        a = eng.adjoint(torch.from_numpy(f[lo:hi]))
+        work.wait()
         q.put((rank, lo, f_loc.numpy(), a.numpy()))
     except Exception as exc:  # surface worker failures instead of a queue timeout
         q.put((rank, None, repr(exc), None))
