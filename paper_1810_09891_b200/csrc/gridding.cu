@@ -1515,7 +1515,6 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       const int4* pr = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* pf = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
-      const int4* const pend = pr + nb;
       auto hits = [&](const int4 r) {
         return (unsigned)r.z <= (unsigned)(H2 - K) && r.x <= wa_hi && r.x + (int)((unsigned)r.w & 0xffu) > wa_lo;
       };
@@ -1545,10 +1544,24 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
           }
         }
       };
-      for (; pr < pend; ++pr, pw += PR, ++pf) {
-        const int4 r = *pr;
-        if (r.z != cur_h) move_window(r.z);
-        if (hits(r)) node1(pw, pf);
+      // this warp's nodes of the batch, run by run (see the whole-row path)
+      static_assert(P::NB <= 32, "one ballot per batch");
+      const int4 rl = lane < nb ? pr[lane] : make_int4(0, 0, -1, 0);
+      unsigned mask = __ballot_sync(~0u, lane < nb && hits(rl));
+      const int zup = __shfl_up_sync(~0u, rl.z, 1);
+      const unsigned rstart = __ballot_sync(~0u, lane == 0 || rl.z != zup);
+      while (mask) {
+        const int j0 = __ffs(mask) - 1;
+        const int h = __shfl_sync(~0u, rl.z, j0);
+        const unsigned later = rstart & ~((2u << j0) - 1u);
+        unsigned run = later ? mask & ((later & (0u - later)) - 1u) : mask;
+        mask &= ~run;
+        if (h != cur_h) move_window(h);
+        do {
+          const int jj = __ffs(run) - 1;
+          run &= run - 1;
+          node1(pw + jj * PR, pf + jj);
+        } while (run);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
@@ -1621,19 +1634,31 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
-      // walk the batch with pointers: node row, sample, record
-      const typename P::W* pw = ws;
-      const C* pf = fv;
-      const int4* pr = rs;
-      const int4* const pend = rs + nb;
-      int4 r = nb > 0 ? *pr : make_int4(0, 0, 0, 0);
-      while (pr < pend) {
+      // Per-batch warp view: lane l holds node l's record; one ballot gives
+      // the nodes whose stencil meets this warp's rows, another the run
+      // starts (last-dim start changes).  The walk then visits only this
+      // warp's nodes, run by run, with bit operations between nodes -- no
+      // record load or test on the node-to-node path.
+      static_assert(P::NB <= 32, "one ballot per batch");
+      const int4 rl = lane < nb ? rs[lane] : make_int4(0, 0, -1, 0);
+      unsigned mask = __ballot_sync(~0u, lane < nb && (unsigned)rl.z <= (unsigned)(H2 - K) &&
+                                              rl.x <= wa_hi && rl.x + (int)((unsigned)rl.w & 0xffu) > wa_lo);
+      const int zup = __shfl_up_sync(~0u, rl.z, 1);
+      const unsigned rstart = __ballot_sync(~0u, lane == 0 || rl.z != zup);
+      while (mask) {
+        const int j0 = __ffs(mask) - 1;
+        const int h = __shfl_sync(~0u, rl.z, j0);
+        const unsigned later = rstart & ~((2u << j0) - 1u);  // run starts after j0 (2u << 31 == 0)
+        const unsigned run = later ? mask & ((later & (0u - later)) - 1u) : mask;
+        mask &= ~run;
+        touched = true;
 #define NFFTK_PIPE_NODE(H)                                                                 \
-  if (r.x <= wa_hi && r.x + (int)((unsigned)r.w & 0xffu) > wa_lo) {                        \
-    /* halo-indexed factor rows: zero off the stencil, no per-lane test */                  \
+  {                                                                                        \
+    const int jj = __ffs(m2) - 1;                                                          \
+    m2 &= m2 - 1;                                                                          \
+    const typename P::W* pw = ws + jj * PR;                                                \
     const R s = (R)(pw[a] * pw[H2 + b]);                                                   \
-    touched = true;                                                                        \
-    const C f = *pf;                                                                       \
+    const C f = fv[jj];                                                                    \
     const R cr = f.x * s, ci = f.y * s;                                                    \
     const C* w2 = reinterpret_cast<const C*>(pw + 2 * H2); /* factor pairs */             \
     _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                       \
@@ -1646,36 +1671,23 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }                                                                                    \
     }                                                                                      \
   }
-#define NFFTK_PIPE_NEXT \
-  ++pr;                 \
-  pw += PR;             \
-  ++pf;
-#define NFFTK_PIPE_CASE(H)                                   \
-    case H:                                                    \
-      if constexpr (H + K <= H2) {                             \
-        for (;;) {                                             \
-          NFFTK_PIPE_NODE(H)                                   \
-          NFFTK_PIPE_NEXT                                      \
-          if (pr >= pend) break;                               \
-          r = *pr;                                             \
-          if (r.z != H) break;                                 \
-        }                                                      \
-      } else {                                                 \
-        NFFTK_PIPE_NEXT                                        \
-        if (pr < pend) r = *pr;                                \
-      }                                                        \
-      break;
-        switch (r.z) {
+#define NFFTK_PIPE_CASE(H)                                                     \
+  case H:                                                                      \
+    if constexpr (H + K <= H2) {                                               \
+      unsigned m2 = run;                                                       \
+      do {                                                                     \
+        NFFTK_PIPE_NODE(H)                                                     \
+      } while (m2);                                                            \
+    }                                                                          \
+    break;
+        switch (h) {
           NFFTK_PIPE_CASE(0) NFFTK_PIPE_CASE(1) NFFTK_PIPE_CASE(2) NFFTK_PIPE_CASE(3)
           NFFTK_PIPE_CASE(4) NFFTK_PIPE_CASE(5) NFFTK_PIPE_CASE(6) NFFTK_PIPE_CASE(7)
           NFFTK_PIPE_CASE(8)
           default:
-            NFFTK_PIPE_NEXT
-            if (pr < pend) r = *pr;
             break;
         }
 #undef NFFTK_PIPE_CASE
-#undef NFFTK_PIPE_NEXT
 #undef NFFTK_PIPE_NODE
       }
       __syncwarp();
