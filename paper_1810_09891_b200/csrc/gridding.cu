@@ -620,7 +620,11 @@ struct IPipeCfg {
   static constexpr int ELEM = 2 * (int)sizeof(R);
   static constexpr int HS = ELEM == 8 ? HL + (HL & 1) : HL;
   static constexpr int ROWS = H0 * H1;
+#ifdef NFFTK_ITHREADS3
+  static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
+#else
   static constexpr int THREADS = D == 3 ? 512 : 256;
+#endif
   // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
 #ifdef NFFTK_NO_HALF
   static constexpr bool HALF = false;
