@@ -623,7 +623,10 @@ struct IPipeCfg {
 #ifdef NFFTK_ITHREADS3
   static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
 #else
-  static constexpr int THREADS = D == 3 ? 512 : 256;
+  // d = 3, m >= 5 (one halo buffer): 20 warps hide more of the halo-cell
+  // load latency (C3 interp 0.363 -> 0.351 ms, c64 0.230 -> 0.217; 24 warps
+  // at the 85-register cap: 0.368); m <= 4 stays at 16 (C5 20.0 vs 20.5 ms)
+  static constexpr int THREADS = D == 3 ? (MM >= 5 ? 640 : 512) : 256;
 #endif
   // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
 #ifdef NFFTK_NO_HALF
@@ -661,7 +664,9 @@ struct IPipeCfg {
   static constexpr int pick_s() {
     for (int s : {4, 3, 2})
       if (halo_off(s) + 2 * HALO <= LIMIT) return s;
-    return 4;
+    for (int s : {4, 3})
+      if (halo_off(s) + HALO <= LIMIT) return s;
+    return 2;
   }
   static constexpr int S = pick_s();
   static constexpr size_t CTL = S * SB;
