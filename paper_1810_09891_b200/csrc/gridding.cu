@@ -458,7 +458,9 @@ __device__ __forceinline__ void interp_node3_sched(const double2* __restrict__ h
 #pragma unroll
   for (int t = 0; t < WF; ++t) w2r[t] = wl[t];
   const double2* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
-#pragma unroll 3
+  // fully unrolled: sch[] stays in registers (a partial unroll indexed it
+  // from local memory: C3 interp 0.351 -> 0.343 ms, c64 0.217 -> 0.208)
+#pragma unroll
   for (int k = 0; k < NIT; ++k) {
     const unsigned e = sch[k];
     if (e == 0xffffu) continue;
@@ -494,7 +496,7 @@ __device__ __forceinline__ void interp_node3_half(const float2* __restrict__ hal
 #pragma unroll
   for (int t = 0; t < MM; ++t) w2r[t] = wl[2 * t + par];
   const float2* corner = halo + (q[0] * H1 + q[1]) * HS + q[2] + par;
-#pragma unroll 3
+#pragma unroll
   for (int k = 0; k < NIT; ++k) {
     const unsigned e = sch[k];
     if (e == 0xffffu) continue;
