@@ -320,7 +320,7 @@ def main():
     peaks = measured_peaks()
     fp64, fp32 = ctypes_fma_peaks(_lib)
     roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32,
-                    tuple(plan.tile), args.psi)
+                    tuple(plan.tile), args.psi, sm_mhz=clk.get("sm_mhz") or clk.get("sm_max_mhz"))
 
     if rank != 0:
         if world > 1:
@@ -479,7 +479,25 @@ BINDING = {
 }
 
 
-def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None):
+def smem_roof(w, s, per_ms, sm_mhz):
+    """The gather's on-chip roof: it reads one s-byte halo cell per node-cell
+    from shared memory ((2m)^d M cells per launch), against the SMs' shared-
+    memory bandwidth of 128 B per clock each (one wavefront) at the SM clock
+    sampled during the timed region."""
+    import torch
+
+    if not sm_mhz or not torch.cuda.is_available():
+        return None
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    alg = (2 * w.m) ** w.d * w.M * s
+    achieved = alg / (per_ms * 1e-3) / 1e12
+    peak = sms * 128 * sm_mhz * 1e6 / 1e12
+    return {"achieved": achieved, "peak": peak, "unit": "TB/s", "frac": achieved / peak,
+            "algorithmic_bytes_per_launch": alg,
+            "peak_source": f"{sms} SMs x 128 B/clk x {sm_mhz:.0f} MHz (sampled SM clock)"}
+
+
+def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None, sm_mhz=None):
     """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
     M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
     (4 w^d M flops with w = 2m).  Times are CUDA-event durations of the kernel
@@ -506,6 +524,8 @@ def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None):
                     "flops_per_launch": flops,
                     "peak_source": "k_fma_peak microbenchmark (measured in run)"},
         }
+        if ph == "interp":
+            out[ph]["smem"] = smem_roof(w, s, per, sm_mhz)
     if not out:
         return None
     dom = max(out, key=lambda k: out[k]["avg_launch_ms"])
