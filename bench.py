@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--reduce", default="fhat", choices=["fhat", "grid"],
                     help="adjoint exchange at N>1: all-reduce the coefficients or the n-grid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of one CUDA-graph replay per step")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -70,6 +72,8 @@ def config_json(w, args, world):
         "adjoint_exchange": "none (1 rank)" if world == 1 else
         f"NCCL all-reduce of the {'coefficients (|I_N|)' if args.reduce == 'fhat' else 'n-grid (|I_n|)'}",
         "l2": "flushed (256 MiB write) before every timed step",
+        "launch": "eager" if getattr(args, "no_graph", False) or world > 1
+        else "CUDA graph of the step (captured once, replayed per step)",
     }
 
 
@@ -273,6 +277,24 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # One rank: the step's launches (deconv, cuFFT, pad, gather, zero,
+    # permute, spread, cuFFT, pack) are captured once into a CUDA graph and
+    # replayed, so the device does not idle between launches.  The library
+    # launches on the caller's (capturing) stream; its ticket counters reset
+    # themselves, so a replay is the same work as an eager step.
+    run, launches_per_step = step, None
+    plan.set_timing(False)
+    if world == 1 and not args.no_graph:
+        l0 = nf.launch_count()
+        step()
+        torch.cuda.synchronize()
+        launches_per_step = nf.launch_count() - l0
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        run = graph.replay
 
     # ---- device-timed region (no per-phase instrumentation inside it)
     plan.set_timing(False)
@@ -289,12 +311,14 @@ def main():
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        step()
+        run()
         b.record(stream)
         b.synchronize()
         total_ms += a.elapsed_time(b)
     torch.cuda.synchronize()
     launches = nf.launch_count() - launches0
+    if launches_per_step is not None:  # graph replays: the host counter does not see them
+        launches = launches_per_step * args.steps
     clk = clocks.stop()
     # ---- the same steps again with per-phase CUDA events (breakdown, roofline)
     plan.phase_times(reset=True)

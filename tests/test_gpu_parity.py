@@ -186,6 +186,63 @@ def test_device_path_equals_host_path(torch):
     assert np.array_equal(q.trafo(c["fhat"]), fh_host)
 
 
+@pytest.mark.parametrize("name", ["d3_m6", "d2_m8", "d1_m8"])
+def test_cuda_graph_replay_matches_reference(name, torch):
+    """trafo + adjoint captured once into a CUDA graph (as bench.py times the
+    step) and replayed on new inputs copied into the captured buffers: the
+    replay matches the reference goldens (ticket counters reset themselves)."""
+    c = case(name)
+    dev = torch.device("cuda", 0)
+    p = make_plan(c)
+    fh = torch.zeros(int(np.prod(c["N"])), dtype=torch.complex128, device=dev)
+    fs = torch.zeros(c["x"].shape[0], dtype=torch.complex128, device=dev)
+    f_out = torch.empty_like(fs)
+    a_out = torch.empty_like(fh)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        p.trafo(fh, out=f_out)
+        p.adjoint(fs, out=a_out)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        p.trafo(fh, out=f_out)
+        p.adjoint(fs, out=a_out)
+    for _ in range(2):
+        fh.copy_(torch.from_numpy(c["fhat"].ravel()))
+        fs.copy_(torch.from_numpy(c["f"].ravel()))
+        g.replay()
+        torch.cuda.synchronize()
+        assert e2(c["trafo"], f_out.cpu().numpy()) < TOL128
+        assert e2(c["adjoint"], a_out.cpu().numpy()) < TOL128
+
+
+def test_cuda_graph_replay_c3_equals_eager(torch):
+    """At the headline workload (persistent gridding kernels with dynamic
+    subproblem tickets): graph replays give the eager trafo bit for bit and
+    the eager adjoint to rounding (fp64 reductions in flush order)."""
+    w = wl.CONFIGS["C3"]
+    dev = torch.device("cuda", 0)
+    p = nf.Plan(w.N, w.M, n=w.n, m=w.m)
+    p.x = torch.from_numpy(wl.nodes(w)).to(dev)
+    p.precompute()
+    fh = torch.from_numpy(wl.fhat(w)).to(dev)
+    fs = torch.from_numpy(wl.samples(w)).to(dev)
+    f_ref = p.trafo(fh).clone()
+    a_ref = p.adjoint(fs).clone()
+    f_out = torch.empty_like(f_ref)
+    a_out = torch.empty_like(a_ref)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        p.trafo(fh, out=f_out)
+        p.adjoint(fs, out=a_out)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(f_out, f_ref)
+        assert e2(a_ref.cpu().numpy(), a_out.cpu().numpy()) < 1e-14
+
+
 def test_trafo_deterministic_adjoint_stable():
     c = case("d3_m6")
     p = make_plan(c)
