@@ -20,6 +20,7 @@ namespace nfftk {
 static unsigned long long g_launches = 0;  // kernels launched by this library
 unsigned long long launch_count() { return g_launches; }
 void count_launch() { ++g_launches; }
+void add_launches(unsigned long long n) { g_launches += n; }
 
 // cells per segment when a line of len cells is cut into nseg warp-sized pieces
 __host__ __device__ inline int seg_width(int len, int nseg) {

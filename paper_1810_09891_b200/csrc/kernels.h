@@ -25,6 +25,7 @@ struct DeconvGeomH {
 
 unsigned long long launch_count();
 void count_launch();
+void add_launches(unsigned long long n);
 int spread_threads(const Geom& g);
 
 void launch_check_range(const double* x, int64_t count, unsigned long long* first_bad,

@@ -123,6 +123,8 @@ Plan::~Plan() {
   if (!grid_external) cudaFree(grid);
   cudaFree(gp);
   cudaFree(sched);
+  for (auto& h : hgraph)
+    if (h.exec) cudaGraphExecDestroy(h.exec);
   cudaFree(fhat_dev);
   cudaFree(f_dev);
   cudaFree(f_sorted);
@@ -421,6 +423,7 @@ static void invalidate_tables(Plan* p) {
 }
 
 void plan_set_nodes_host(Plan* p, const double* x, int64_t len) {
+  ++p->gen;
   shape_check_x(p, len);
   check_range_host(p, x);
   std::vector<double> copy(x, x + p->M * p->d);
@@ -441,6 +444,7 @@ void plan_set_nodes_host(Plan* p, const double* x, int64_t len) {
 }
 
 void plan_set_nodes_device(Plan* p, const double* x, int64_t len, cudaStream_t s) {
+  ++p->gen;
   shape_check_x(p, len);
   if (p->d > MAX_D) fail(EK_SHAPE, "fast transforms support d <= 3, got d=" + std::to_string(p->d));
   NFFTK_CUDA(cudaSetDevice(p->device));
@@ -532,6 +536,7 @@ static void ensure_grid(Plan* p) {
 
 void plan_precompute(Plan* p, cudaStream_t s) {
   if (!p->has_nodes) fail(EK_STATE, "set nodes before precompute()");
+  ++p->gen;
   if (p->d > MAX_D) {
     // plan.py:278-279: full tables are limited to d <= 3; others only need host tables
     if (p->f1 & PRE_FULL_PSI)
@@ -692,32 +697,101 @@ static void ensure_io(Plan* p) {
   if (!p->f_dev) NFFTK_CUDA(cudaMalloc(&p->f_dev, p->elem_bytes() * p->M));
 }
 
-void plan_trafo_host(Plan* p, const void* fhat, void* f) {
-  require_ready(p);
-  ensure_stream(p);
-  ensure_io(p);
-  cudaStream_t s = p->own_stream;
+static bool is_pinned(const void* h) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static void trafo_host_body(Plan* p, const void* fhat, void* f, cudaStream_t s) {
   { PhaseScope ps(p, PH_H2D, s);
     NFFTK_CUDA(cudaMemcpyAsync(p->fhat_dev, fhat, p->elem_bytes() * p->num_freqs,
                                cudaMemcpyHostToDevice, s)); }
   plan_trafo_device(p, p->fhat_dev, p->f_dev, s);
   { PhaseScope ps(p, PH_D2H, s);
     NFFTK_CUDA(cudaMemcpyAsync(f, p->f_dev, p->elem_bytes() * p->M, cudaMemcpyDeviceToHost, s)); }
-  NFFTK_CUDA(cudaStreamSynchronize(s));
 }
 
-void plan_adjoint_host(Plan* p, const void* f, void* fhat) {
-  require_ready(p);
-  ensure_stream(p);
-  ensure_io(p);
-  cudaStream_t s = p->own_stream;
+static void adjoint_host_body(Plan* p, const void* f, void* fhat, cudaStream_t s) {
   { PhaseScope ps(p, PH_H2D, s);
     NFFTK_CUDA(cudaMemcpyAsync(p->f_dev, f, p->elem_bytes() * p->M, cudaMemcpyHostToDevice, s)); }
   plan_adjoint_device(p, p->f_dev, p->fhat_dev, s);
   { PhaseScope ps(p, PH_D2H, s);
     NFFTK_CUDA(cudaMemcpyAsync(fhat, p->fhat_dev, p->elem_bytes() * p->num_freqs,
                                cudaMemcpyDeviceToHost, s)); }
+}
+
+// Runs body eagerly, or through the plan's captured graph for this
+// direction: the first call with a given (in, out, plan state) runs eagerly
+// (one-time allocations and attribute setup happen there), the second
+// captures and launches the graph, later ones only launch it.  Pinned host
+// buffers only (a graph's memcpy nodes need them); phase timing runs eagerly.
+template <typename Body>
+static void host_call(Plan* p, int dir, const void* in, void* out, Body body) {
+  cudaStream_t s = p->own_stream;
+  Plan::HostGraph& h = p->hgraph[dir];
+  const bool same = h.in == in && h.out == out && h.gen == p->gen;
+  if (!same) {
+    if (h.exec) cudaGraphExecDestroy(h.exec);
+    h = Plan::HostGraph();
+    h.in = in;
+    h.out = out;
+    h.gen = p->gen;
+  }
+  const bool usable = !p->graphs_off && !p->timing && !getenv("NFFTK_NO_HOST_GRAPH") &&
+                      is_pinned(in) && is_pinned(out);
+  if (usable && !h.exec && h.seen >= 1) {
+    const unsigned long long l0 = launch_count();
+    cudaGraph_t graph = nullptr;
+    NFFTK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      body(s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      throw;
+    }
+    NFFTK_CUDA(cudaStreamEndCapture(s, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {  // keep the eager launches for this plan
+      cudaGetLastError();
+      p->graphs_off = true;
+    } else {
+      h.exec = exec;
+      h.launches = launch_count() - l0;
+      add_launches(0ull - h.launches);  // the capture itself launched nothing
+    }
+  }
+  ++h.seen;
+  if (usable && h.exec) {
+    NFFTK_CUDA(cudaGraphLaunch(h.exec, s));
+    add_launches(h.launches);
+    count_evals(p);  // the host-side counter update the captured call made once
+  } else {
+    body(s);
+  }
   NFFTK_CUDA(cudaStreamSynchronize(s));
+}
+
+void plan_trafo_host(Plan* p, const void* fhat, void* f) {
+  require_ready(p);
+  ensure_stream(p);
+  ensure_io(p);
+  host_call(p, 0, fhat, f, [&](cudaStream_t s) { trafo_host_body(p, fhat, f, s); });
+}
+
+void plan_adjoint_host(Plan* p, const void* f, void* fhat) {
+  require_ready(p);
+  ensure_stream(p);
+  ensure_io(p);
+  if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * (p->M + 2)));
+  host_call(p, 1, f, fhat, [&](cudaStream_t s) { adjoint_host_body(p, f, fhat, s); });
 }
 
 void plan_node_order(Plan* p, int64_t* out) {
@@ -742,6 +816,7 @@ void plan_bind_grid(Plan* p, void* dev, int64_t bytes) {
   if (p->grid && !p->grid_external) cudaFree(p->grid);
   p->grid = dev;
   p->grid_external = true;
+  ++p->gen;
 }
 
 }  // namespace nfftk

@@ -77,6 +77,23 @@ struct Plan {
   double* f_host = nullptr;
   bool fhat_pinned = false, f_pinned = false;
 
+  // ---- host-path CUDA graphs (plan_trafo_host / plan_adjoint_host): the
+  // H2D copy, the transform's launches and the D2H copy, captured on the
+  // second call with the same buffers and plan state, then one
+  // cudaGraphLaunch per call.  gen counts the plan-state changes (nodes,
+  // tables, grid) that invalidate a captured graph.
+  struct HostGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* in = nullptr;
+    void* out = nullptr;
+    uint64_t gen = ~0ull;
+    int seen = 0;
+    unsigned long long launches = 0;
+  };
+  HostGraph hgraph[2];  // 0: trafo, 1: adjoint
+  bool graphs_off = false;
+  uint64_t gen = 0;
+
   // ---- instrumentation
   bool timing = false;
   struct Rec { int phase; cudaEvent_t a, b; };

@@ -293,6 +293,42 @@ def test_abi_matches_python_api_bitwise():
     assert lib.nfftk_destroy(h) == 0
 
 
+def test_abi_host_graph_replays_and_invalidation(oracle):
+    """C-ABI calls on >= 1 MiB (pinned, library-owned) buffers run through a
+    per-plan CUDA graph from the second call on: repeated calls reproduce the
+    first, new nodes (set_x) invalidate the graph, results match the oracle."""
+    N, n, m, M = (256, 256), (512, 512), 8, 65536
+    rng = np.random.default_rng(5)
+    lib = _lib.load()
+    h = lib.nfftk_create_advanced(_lib.i32_array(N), 2, M, _lib.i32_array(n), m, 0x1fd1, 0x41)
+    assert h > 0
+    K = N[0] * N[1]
+    fhc = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+    fsc = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    fview = np.ctypeslib.as_array(ctypes.cast(lib.nfftk_get_f(h), ctypes.POINTER(ctypes.c_double)),
+                                  (2 * M,)).view(np.complex128)
+    aview = np.ctypeslib.as_array(ctypes.cast(lib.nfftk_get_fhat(h), ctypes.POINTER(ctypes.c_double)),
+                                  (2 * K,)).view(np.complex128)
+    for seed in (11, 12):
+        x = np.ascontiguousarray(np.random.default_rng(seed).random((M, 2)) - 0.5)
+        assert lib.nfftk_set_x(h, x.ctypes.data, x.size) == 0
+        outs, adjs = [], []
+        for _ in range(3):
+            fh = np.ascontiguousarray(fhc).view(np.float64)
+            assert lib.nfftk_set_fhat(h, fh.ctypes.data, fh.size) == 0
+            assert lib.nfftk_trafo(h) == 0
+            outs.append(fview.copy())
+            fs = np.ascontiguousarray(fsc).view(np.float64)
+            assert lib.nfftk_set_f(h, fs.ctypes.data, fs.size) == 0
+            assert lib.nfftk_adjoint(h) == 0
+            adjs.append(aview.copy())
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+        assert e2(adjs[0], adjs[2]) < 1e-14
+        assert e2(oracle.trafo(N, n, m, x, fhc), outs[2]) < TOL128
+        assert e2(oracle.adjoint(N, n, m, x, fsc), adjs[2]) < TOL128
+    assert lib.nfftk_destroy(h) == 0
+
+
 def test_abi_rank4_quirks():
     """Reference quirks (SURVEY 8(b)): rank-4 set_x succeeds, trafo -> -2;
     rank-4 with PRE_FULL_PSI -> set_x -9."""
