@@ -72,7 +72,8 @@ def config_json(w, args, world):
         "adjoint_exchange": "none (1 rank)" if world == 1 else
         f"NCCL all-reduce of the {'coefficients (|I_N|)' if args.reduce == 'fhat' else 'n-grid (|I_n|)'}",
         "l2": "flushed (256 MiB write) before every timed step",
-        "launch": "eager" if getattr(args, "no_graph", False) or world > 1
+        "launch": "host CPU (reference arm)" if getattr(args, "impl", "ours") == "reference"
+        else "eager" if getattr(args, "no_graph", False) or world > 1
         else "CUDA graph of the step (captured once, replayed per step)",
     }
 
