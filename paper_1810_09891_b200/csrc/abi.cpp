@@ -106,7 +106,9 @@ double* alloc_host(int64_t doubles, bool* pinned) {
   size_t bytes = sizeof(double) * (size_t)(doubles > 0 ? doubles : 1);
   void* ptr = nullptr;
   *pinned = false;
-  if (bytes >= (1 << 20) && cudaHostAlloc(&ptr, bytes, cudaHostAllocPortable) == cudaSuccess) {
+  // pinned at every size: copies run at PCIe rate and the host calls can
+  // replay their CUDA graph (plan.cu host_call needs pinned buffers)
+  if (cudaHostAlloc(&ptr, bytes, cudaHostAllocPortable) == cudaSuccess) {
     *pinned = true;
     memset(ptr, 0, bytes);
     return (double*)ptr;
