@@ -291,9 +291,28 @@ __global__ void k_gather_subs(const int4* __restrict__ subs, const int* __restri
   if (i < total) out[i] = subs[order[i]];
 }
 
+// The sort's temporaries come from the device's default stream-ordered pool;
+// with its default release threshold (0) every synchronisation hands the
+// memory back and the next set_nodes maps it again (~60 us per
+// cudaMallocAsync).  Keep what the pool holds (at most the largest set_nodes'
+// temporaries: keys, values, CUB workspace).
+static void keep_pool_memory() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[dev] = true;
+}
+
 void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int ntiles,
                   int* perm, double* xs, int* tile_count, int* tile_start, int4** subs,
                   int* nsubs, cudaStream_t s) {
+  keep_pool_memory();
   uint32_t *keys = nullptr, *keys2 = nullptr;
   int *vals = nullptr, *nsub = nullptr, *sub_start = nullptr;
   NFFTK_CUDA(cudaMallocAsync(&keys, sizeof(uint32_t) * M * 2, s));
