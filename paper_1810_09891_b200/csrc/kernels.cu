@@ -168,40 +168,49 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
 // (the rows of consecutive sorted nodes are adjacent).  The per-entry kernel
 // above re-derived the stencil for every table entry, zeros included.
 constexpr int PSI_NODES = 64;
+constexpr int PSI_STENCIL_BYTES = PSI_NODES * MAX_D * (8 + 4 + 4);
 template <typename T>
 __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict__ xs, int64_t M, Geom g,
                                                         T* __restrict__ psi) {
   extern __shared__ __align__(16) unsigned char psm[];
-  T* tile = reinterpret_cast<T*>(psm);
+  // per (node, dim) stencil, formed once: lo, row position of offset 0, width
+  int64_t* slo = reinterpret_cast<int64_t*>(psm);
+  int* spos = reinterpret_cast<int*>(slo + PSI_NODES * MAX_D);
+  int* swid = spos + PSI_NODES * MAX_D;
+  T* tile = reinterpret_cast<T*>(psm + PSI_STENCIL_BYTES);
   const int K = 2 * g.m + 1, pr = g.pr;
   const int64_t i0 = (int64_t)blockIdx.x * PSI_NODES;
   const int nn = (int)min((int64_t)PSI_NODES, M - i0);
   for (int e = threadIdx.x; e < nn * pr; e += blockDim.x) tile[e] = (T)0;
-  __syncthreads();
-  const int items = nn * g.d * K;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int t = it % K;
-    const int nd = it / K;
+  for (int nd = threadIdx.x; nd < nn * g.d; nd += blockDim.x) {
     const int dim = nd % g.d, j = nd / g.d;
-    const double x = xs[dim * M + i0 + j];
-    const Stencil st = stencil(x, g.nd[dim], g.md);
-    if (t >= st.width) continue;
-    int pos = dim * K + t;
+    const Stencil st = stencil(xs[dim * M + i0 + j], g.nd[dim], g.md);
+    int pos = dim * K;
     if (g.psi_pad) {
       // halo-indexed leading dims (stencil offset t at halo cell h + t), then
       // the last dim's 2m+1 factors -- k_build_psi's layout
       int off = 0;
       for (int e = 0; e < dim; ++e) off += g.H[e];
+      pos = off;
       if (dim + 1 < g.d) {
         const int64_t slot = floor_mod(st.cell, g.n[dim]);
         const int tcoord = (int)(slot / g.T[dim]);
-        const int h = (int)(slot - (int64_t)tcoord * g.T[dim]) + g.m - (int)(st.cell - st.lo);
-        pos = off + h + t;
-      } else {
-        pos = off + t;
+        pos += (int)(slot - (int64_t)tcoord * g.T[dim]) + g.m - (int)(st.cell - st.lo);
       }
     }
-    tile[j * pr + pos] = (T)(dim_factor(g, dim, x, st.lo + t) * g.wscale[dim]);
+    slo[nd] = st.lo;
+    spos[nd] = pos;
+    swid[nd] = st.width;
+  }
+  __syncthreads();
+  const int items = nn * g.d * K;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int t = it % K;
+    const int nd = it / K;
+    if (t >= swid[nd]) continue;
+    const int dim = nd % g.d, j = nd / g.d;
+    const double x = xs[dim * M + i0 + j];
+    tile[j * pr + spos[nd] + t] = (T)(dim_factor(g, dim, x, slo[nd] + t) * g.wscale[dim]);
   }
   __syncthreads();
   T* out = psi + i0 * pr;
@@ -209,7 +218,8 @@ __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict
 }
 
 void build_psi(const double* xs, int64_t M, const Geom& g, void* psi, cudaStream_t s) {
-  const size_t smem = (size_t)PSI_NODES * g.pr * (g.psi_f32 ? sizeof(float) : sizeof(double));
+  const size_t smem =
+      PSI_STENCIL_BYTES + (size_t)PSI_NODES * g.pr * (g.psi_f32 ? sizeof(float) : sizeof(double));
   const unsigned blocks = (unsigned)((M + PSI_NODES - 1) / PSI_NODES);
   if (getenv("NFFTK_PSI_PER_ENTRY") || smem > 48 * 1024 || blocks == 0) {
     if (g.psi_f32)
