@@ -1645,12 +1645,30 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     }
   }
   } else {
-  const int row = threadIdx.x;
+  const int row = threadIdx.x;       // also this thread's staging slot
   const bool owner = row < P::ROWS;  // non-owners accumulate garbage that is never flushed
-  const int a = owner ? row / H2 : 0, b = owner ? row % H2 : 0;
-  const int wa_lo = min((int)(threadIdx.x & ~31u), P::ROWS - 1) / H2;
-  const int wa_hi = min((int)(threadIdx.x | 31u), P::ROWS - 1) / H2;
+#ifdef NFFTK_NO_ALT_ROWS
+  constexpr int SH = 0;
+#else
+  // Alternating row maps: on odd tiles a thread holds halo row (row + SH) mod
+  // ROWS, about half a halo further on, so a warp that owns well-covered
+  // centre a-lines on one tile owns thinly covered edge lines on the next.
+  // The node ring (S - 1 stages ahead) lets fast warps run into the next
+  // tile, so over a pair of tiles every warp does about the same work
+  // instead of the centre warps setting the pace of every tile.
+  constexpr int SH = P::ROWS / 2;
+#endif
+  int tpar = 0;
   for (;;) {  // tiles of this CTA
+    const int shift = tpar ? SH : 0;
+    tpar ^= 1;
+    const int rr = owner ? (row + shift) % P::ROWS : 0;
+    const int a = rr / H2, b = rr % H2;
+    // this warp's a-lines: one interval, or two when its rows wrap
+    const int w0 = (int)(threadIdx.x & ~31u), w1 = min((int)(threadIdx.x | 31u), P::ROWS - 1);
+    const int s0 = (w0 + shift) % P::ROWS, s1 = (w1 + shift) % P::ROWS;
+    const int wa_lo = s0 / H2, wa_hi = s0 <= s1 ? s1 / H2 : H2 - 1;
+    const int wb_lo = s0 <= s1 ? (1 << 20) : 0, wb_hi = s0 <= s1 ? -1 : s1 / H2;
     R accr[H2], acci[H2];
 #pragma unroll
     for (int c = 0; c < H2; ++c) accr[c] = acci[c] = 0;
@@ -1674,8 +1692,10 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       // record load or test on the node-to-node path.
       static_assert(P::NB <= 32, "one ballot per batch");
       const int4 rl = lane < nb ? rs[lane] : make_int4(0, 0, -1, 0);
+      const int rw0 = (int)((unsigned)rl.w & 0xffu);
       unsigned mask = __ballot_sync(~0u, lane < nb && (unsigned)rl.z <= (unsigned)(H2 - K) &&
-                                              rl.x <= wa_hi && rl.x + (int)((unsigned)rl.w & 0xffu) > wa_lo);
+                                              ((rl.x <= wa_hi && rl.x + rw0 > wa_lo) ||
+                                               (rl.x <= wb_hi && rl.x + rw0 > wb_lo)));
       const int zup = __shfl_up_sync(~0u, rl.z, 1);
       const unsigned rstart = __ballot_sync(~0u, lane == 0 || rl.z != zup);
       while (mask) {
