@@ -15,8 +15,9 @@ One step = one forward transform (D -> F -> B) plus one adjoint
                threads, bounded sample, rank 0 at N=1.
 
 ``--impl reference`` times only that CPU port (rank 0; other ranks exit 0).
-Multi-GPU (torchrun): weak scaling, each rank owns M nodes of one plan; the
-adjoint all-reduces the spread grid with NCCL (paper_1810_09891_b200.distributed).
+Multi-GPU (torchrun): strong scaling -- the configuration's M nodes are split
+across the ranks in tile order; the exchange (default: slab-decomposed F with
+NCCL all-to-all, paper_1810_09891_b200.distributed) runs inside the step.
 """
 
 import argparse
@@ -35,7 +36,10 @@ sys.path.insert(0, ROOT)
 
 from paper_1810_09891_b200 import workloads as wl  # noqa: E402
 
-DEFAULT_CONFIG = "C3"
+# The headline workload: the largest BASELINE configuration that fits one
+# GPU (C5: d=3, 512^3 grid, M = 2^26, complex128); C1-C4 are parity cases
+# with their own bench lines under profiles/.
+DEFAULT_CONFIG = "C5"
 
 
 def parse():
@@ -47,12 +51,12 @@ def parse():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(wl.CONFIGS))
     ap.add_argument("--precision", default="double", choices=["double", "single"])
     ap.add_argument("--psi", default="flags", choices=["flags", "direct", "tensor"])
-    ap.add_argument("--reduce", default="fhat", choices=["fhat", "grid"],
-                    help="adjoint exchange at N>1: all-reduce the coefficients or the n-grid")
+    ap.add_argument("--reduce", default="slab", choices=["fhat", "grid", "slab"],
+                    help="exchange at N>1 (distributed.py): slab-decomposed F with row-block "
+                         "exchange (default; d >= 2), all-reduce of the coefficients, or of the n-grid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of one CUDA-graph replay per step")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
 
@@ -61,21 +65,36 @@ def env_rank():
         int(os.environ.get("LOCAL_RANK", 0))
 
 
+EXCHANGE = {
+    "fhat": "replicated D+F; NCCL all-reduce of the adjoint coefficients (|I_N|)",
+    "grid": "replicated D+F; NCCL all-reduce of the spread n-grid (|I_n|)",
+    "slab": "slab-decomposed F/F^H (NCCL all-to-all transpose), row-block exchange of "
+            "owned slabs + halos, all-reduce of the disjoint coefficient parts",
+}
+
+
 def config_json(w, args, world):
     return {
         "workload": f"{w.name}: d={w.d} N={'x'.join(map(str, w.N))} n={'x'.join(map(str, w.n))} "
-                    f"M={w.M} per rank m={w.m} {w.dist} nodes, Kaiser-Bessel",
-        "d": w.d, "N": list(w.N), "n": list(w.n), "M_per_rank": w.M, "m": w.m,
+                    f"M={w.M} m={w.m} {w.dist} nodes, Kaiser-Bessel",
+        "d": w.d, "N": list(w.N), "n": list(w.n), "M": w.M, "m": w.m,
         "nodes": w.dist, "window": "kaiserbessel", "flags": "default f1 (PRE_PHI_HUT|PRE_PSI|sort)"
         if args.psi == "flags" else f"psi={args.psi}",
-        "step": "trafo + adjoint", "parallelism": f"node-sharded x{world}",
-        "adjoint_exchange": "none (1 rank)" if world == 1 else
-        f"NCCL all-reduce of the {'coefficients (|I_N|)' if args.reduce == 'fhat' else 'n-grid (|I_n|)'}",
+        "step": "trafo + adjoint",
+        "parallelism": "1 GPU" if world == 1 else
+        f"{world} GPUs, nodes sharded by tile order (M/{world} per rank)",
+        "exchange": "none (1 rank)" if world == 1 else EXCHANGE[args.reduce if w.d > 1 else "fhat"],
         "l2": "flushed (256 MiB write) before every timed step",
-        "launch": "host CPU (reference arm)" if getattr(args, "impl", "ours") == "reference"
-        else "eager" if getattr(args, "no_graph", False) or world > 1
-        else "CUDA graph of the step (captured once, replayed per step)",
     }
+
+
+def launch_mode(args, world):
+    """How the step is issued (a property of the arm, not of the workload)."""
+    if getattr(args, "impl", "ours") == "reference":
+        return "host CPU (reference arm)"
+    if getattr(args, "no_graph", False) or world > 1:
+        return "eager"
+    return "CUDA graph of the step (captured once, replayed per step)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -135,45 +154,24 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def cpu_oracle_rate(w, seconds, seed_offset=0):
-    """Time the CPU oracle port (trafo + adjoint) on a bounded node sample.
-
-    The sample keeps the grid, cutoff and node distribution and scales M down
-    until one trafo+adjoint takes a bounded time; the rate is nodes/s of the
-    full step (deconvolution + FFT + gridding) at that M.
-    """
+def cpu_oracle_rate(w, seed_offset=0):
+    """Time the CPU oracle port (trafo + adjoint) on the FULL workload: one
+    step at the configuration's full M and grid (no scaled sample, so the
+    grid-sized work -- deconvolution, FFTs -- is not divided by a small M)."""
     from oracle import oracle as O
 
     O.set_threads(host_cores())
     threads = O.max_threads()
-    M = w.M
-    base = wl.scaled(w, M)
-    # probe with a small sample, then size the measured sample
-    probe = wl.scaled(w, min(M, 16384))
-    x = wl.nodes(probe, seed=wl.NODE_SEED + seed_offset)
-    fh = wl.fhat(probe)
-    fs = wl.samples(probe)
+    x = wl.nodes(w, seed=wl.NODE_SEED + seed_offset)
+    fh = wl.fhat(w)
+    fs = wl.samples(w)
     t0 = time.perf_counter()
     O.trafo(w.N, w.n, w.m, x, fh)
     O.adjoint(w.N, w.n, w.m, x, fs)
-    t_probe = time.perf_counter() - t0
-    target = max(1.0, seconds / 3.0)
-    Ms = M if t_probe * M / probe.M < target else max(probe.M, int(probe.M * target / max(t_probe, 1e-3)))
-    Ms = min(M, Ms)
-    samp = wl.scaled(base, Ms)
-    x = wl.nodes(samp, seed=wl.NODE_SEED + seed_offset)
-    fh = wl.fhat(samp)
-    fs = wl.samples(samp)
-    reps, elapsed = 0, 0.0
-    while reps < 3 and elapsed < seconds:
-        t0 = time.perf_counter()
-        O.trafo(w.N, w.n, w.m, x, fh)
-        O.adjoint(w.N, w.n, w.m, x, fs)
-        elapsed += time.perf_counter() - t0
-        reps += 1
-    rate = Ms * reps / elapsed
-    sample = (f"oracle/ C port (OpenMP) of reference trafo+adjoint, {reps} step(s) at M={Ms}"
-              f" of {M} (same grid/cutoff/distribution), {threads} threads")
+    elapsed = time.perf_counter() - t0
+    rate = w.M / elapsed
+    sample = (f"oracle/ C port (OpenMP) of the reference trafo+adjoint: one step of the full "
+              f"{w.name} workload (M={w.M}, full grid), {elapsed:.1f} s, {threads} threads")
     return rate, threads, sample
 
 
@@ -202,9 +200,10 @@ def run_reference(args):
     line = {
         "metric": "NFFT trafo+adjoint nodes/sec", "value": value, "unit": "nodes/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded, SURVEY 8(d) generators)", "impl": "reference",
         "config": config_json(w, args, 1),
+        "launch": launch_mode(args, 1),
         "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "port",
                          "sample": f"full {w.name} workload (M={w.M}) per step, oracle/ C port "
                                    f"of the reference path, {threads} OpenMP threads"},
@@ -243,13 +242,15 @@ def main():
     cdt = torch.complex64 if args.precision == "single" else torch.complex128
     s_elem = 8 if args.precision == "single" else 16
 
-    # ---- plan over this rank's shard (weak scaling: M nodes per rank)
+    # ---- plan over this rank's shard (strong scaling: the configuration's M
+    # nodes split across the ranks in tile order)
+    reduce = args.reduce if w.d > 1 else "fhat"
     dp = DistributedPlan(w.N, w.M, n=w.n, m=w.m, precision=args.precision, device=dev,
-                         reduce=args.reduce)
+                         reduce=reduce)
     plan = dp.plan
     if args.psi != "flags":
         plan.set_psi_policy(nf.MODE_DIRECT if args.psi == "direct" else nf.MODE_TENSOR)
-    x = torch.from_numpy(wl.nodes(w, seed=wl.NODE_SEED + rank)).to(dev)
+    x = torch.from_numpy(wl.nodes(w)).to(dev)
     # set_nodes + precompute (sort, stencil records, PRE_PSI): the first call
     # includes one-time costs (module loading, buffer allocation); the second,
     # on the same plan, is the steady-state cost the paper reports
@@ -262,9 +263,10 @@ def main():
         torch.cuda.synchronize()
         pre.append(1000 * (time.perf_counter() - t0))
     precompute_cold_ms, precompute_ms = pre
+    del x
     fhat = torch.from_numpy(wl.fhat(w)).to(dev, cdt)
-    fsamp = torch.from_numpy(wl.samples(w, seed=wl.F_SEED + rank)).to(dev, cdt)
-    f_out = torch.empty(w.M, dtype=cdt, device=dev)
+    fsamp = dp.scatter(torch.from_numpy(wl.samples(w)).to(dev, cdt))
+    f_out = torch.empty(dp.M_local, dtype=cdt, device=dev)
     fhat_out = torch.empty(w.num_freqs, dtype=cdt, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -272,7 +274,7 @@ def main():
         # adjoint first: at N > 1 its coefficient all-reduce is in flight
         # while the (independent) trafo runs
         _, work = dp.adjoint(fsamp, out=fhat_out, async_op=True)
-        plan.trafo(fhat, out=f_out)
+        dp.trafo(fhat, out=f_out)
         work.wait()
 
     for _ in range(max(3, args.warmup)):
@@ -336,7 +338,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    value = world * w.M / (ms_per_step / 1000.0)
+    value = w.M / (ms_per_step / 1000.0)
 
     # ---- e2e through the reference-facing C-ABI with host buffers
     e2e = e2e_abi(w, args, rank, world, dp, dev, cdt)
@@ -354,10 +356,11 @@ def main():
     line = {
         "metric": "NFFT trafo+adjoint nodes/sec", "value": value, "unit": "nodes/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c64" if args.precision == "single" else "c128",
         "data": "synthetic (seeded, SURVEY 8(d) generators)",
         "config": config_json(w, args, world),
+        "launch": launch_mode(args, world),
         "e2e": e2e,
         "roofline": roof,
         "gpu_launches": int(launches),
@@ -368,7 +371,7 @@ def main():
         "fma_peaks_tflops": {"fp64": fp64, "fp32": fp32},
     }
     if world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample = cpu_oracle_rate(w, args.cpu_seconds)
+        rate, cores, sample = cpu_oracle_rate(w)
         line["cpu_baseline"] = {"value": rate, "unit": "nodes/s", "cores": cores, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
@@ -389,8 +392,11 @@ def e2e_abi(w, args, rank, world, dp, dev, cdt):
     from paper_1810_09891_b200 import _lib
 
     fh = np.ascontiguousarray(wl.fhat(w)).view(np.float64)
-    fs = np.ascontiguousarray(wl.samples(w, seed=wl.F_SEED + rank)).view(np.float64)
-    h2d = 16 * (w.num_freqs + w.M) if args.precision == "double" else 8 * (w.num_freqs + w.M)
+    fs_all = wl.samples(w)
+    s_el = 16 if args.precision == "double" else 8
+    # whole-job bytes per step: every rank copies the coefficients in and out,
+    # the samples are split across the ranks
+    h2d = s_el * (world * w.num_freqs + w.M)
     d2h = h2d
     steps = max(3, min(args.steps, 10))
     if world == 1 and args.precision == "double":
@@ -402,6 +408,8 @@ def e2e_abi(w, args, rank, world, dp, dev, cdt):
         assert h > 0, h
         x = np.ascontiguousarray(wl.nodes(w))
         assert lib.nfftk_set_x(h, x.ctypes.data, x.size) == 0, lib.nfftk_last_error_message(h)
+
+        fs = np.ascontiguousarray(fs_all).view(np.float64)
 
         def one():
             rc = lib.nfftk_set_fhat(h, fh.ctypes.data, fh.size) or lib.nfftk_trafo(h)
@@ -419,8 +427,8 @@ def e2e_abi(w, args, rank, world, dp, dev, cdt):
         path = "C-ABI nfftk_set_fhat+nfftk_trafo+nfftk_set_f+nfftk_adjoint (host buffers)"
     else:
         fhh = torch.from_numpy(wl.fhat(w)).to(cdt).pin_memory()
-        fsh = torch.from_numpy(wl.samples(w, seed=wl.F_SEED + rank)).to(cdt).pin_memory()
-        fo = torch.empty(w.M, dtype=cdt).pin_memory()
+        fsh = torch.from_numpy(fs_all[dp.shard_index.cpu().numpy()]).to(cdt).pin_memory()
+        fo = torch.empty(dp.M_local, dtype=cdt).pin_memory()
         fho = torch.empty(w.num_freqs, dtype=cdt).pin_memory()
 
         def one():
@@ -443,7 +451,7 @@ def e2e_abi(w, args, rank, world, dp, dev, cdt):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": world * w.M / (ms / 1000.0), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
+    return {"value": w.M / (ms / 1000.0), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "path": path, "steps": steps}
 
 

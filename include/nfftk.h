@@ -152,6 +152,13 @@ int32_t nfftk_ndft_adjoint_device(int32_t handle, const void * f_dev, void * fha
 int32_t nfftk_spread_device(int32_t handle, const void * f_dev, void * stream);
 int32_t nfftk_adjoint_finish_device(int32_t handle, void * fhat_dev, void * stream);
 int32_t nfftk_bind_grid(int32_t handle, void * grid_dev, int64_t bytes);
+/* B alone from the plan's dense n-grid (filled by the caller, e.g. a
+ * distributed F into a bound grid): samples at the plan's nodes on `stream` */
+int32_t nfftk_interp_device(int32_t handle, void * f_dev, void * stream);
+/* the deconvolution column of dim: 1/(phi_hat_dim(k) * wscale) for
+ * k = -N/2 .. N/2-1 (len = N_dim; transform.py:44-54) -- D / D^H of a
+ * distributed F apply it with 1/|I_n| */
+int32_t nfftk_deconv_cols(int32_t handle, int32_t dim, double * out, int64_t len);
 
 /* introspection */
 int32_t nfftk_get_params(int32_t handle, int64_t * out, int32_t count);

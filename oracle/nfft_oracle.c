@@ -343,6 +343,9 @@ static int64_t freq_slot(const oplan *p, int64_t lin, int *kk) {
     return slot;
 }
 
+int oracle_gather_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                       const double *x, const cplx *g, cplx *f);
+
 /* transform.py:92-118 -- f = B F D f_hat */
 int oracle_trafo(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
                  const double *x, const cplx *fhat, cplx *f) {
@@ -359,7 +362,18 @@ int oracle_trafo(int d, const int *N, const int *n, int m, int code, int mode, i
     }
     free_cols(&p, cols);
     oracle_fft_nd(d, n, g, -1);
-    /* kernels.py:122-197 -- prange over nodes, lexicographic accumulation */
+    oracle_gather_grid(d, N, n, m, code, mode, M, x, g, f);
+    free(g);
+    free(p.lut);
+    return 0;
+}
+
+/* kernels.py:122-197 -- B alone: f_j from a given (FFT'd) oversampled grid;
+ * prange over nodes, lexicographic accumulation */
+int oracle_gather_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                       const double *x, const cplx *g, cplx *f) {
+    oplan p;
+    if (setup(&p, d, N, n, m, code, mode)) return -1;
 #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < M; ++j) {
         int64_t w0[64], w1[64], w2[64];
@@ -390,7 +404,6 @@ int oracle_trafo(int d, const int *N, const int *n, int m, int code, int mode, i
         }
         f[j] = acc;
     }
-    free(g);
     free(p.lut);
     return 0;
 }

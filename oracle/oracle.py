@@ -44,6 +44,8 @@ def lib():
         L.oracle_spread_grid.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int,
                                          ctypes.c_int]
+        L.oracle_gather_grid.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int64, vp, vp, vp]
         L.oracle_adjoint_finish.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
                                             vp, vp]
         L.oracle_ndft.argtypes = [ctypes.c_int, i32p, ctypes.c_int64, vp, vp, vp]
@@ -124,6 +126,19 @@ def spread_grid(N, n, m, x, f, window="kaiserbessel", lut=False, blockwise=None,
     if rc:
         raise ValueError("oracle_spread_grid supports d <= 3")
     return g
+
+
+def gather_grid(N, n, m, x, grid, window="kaiserbessel", lut=False):
+    """B alone (kernels.py:122-197): samples at x from a given oversampled grid."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    M, d = x.shape
+    g = np.ascontiguousarray(grid, dtype=np.complex128).ravel()
+    out = np.empty(M, dtype=np.complex128)
+    rc = lib().oracle_gather_grid(d, _ivec(N), _ivec(n), int(m), _kind(window),
+                                  MODE_LUT if lut else MODE_DIRECT, M, _ptr(x), _ptr(g), _ptr(out))
+    if rc:
+        raise ValueError("oracle_gather_grid supports d <= 3")
+    return out
 
 
 def adjoint_finish(N, n, m, grid, window="kaiserbessel"):

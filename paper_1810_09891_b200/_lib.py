@@ -54,6 +54,8 @@ SIGNATURES = {
     "nfftk_spread_device": (_i32, [_i32, _vp, _vp]),
     "nfftk_adjoint_finish_device": (_i32, [_i32, _vp, _vp]),
     "nfftk_bind_grid": (_i32, [_i32, _vp, _i64]),
+    "nfftk_interp_device": (_i32, [_i32, _vp, _vp]),
+    "nfftk_deconv_cols": (_i32, [_i32, _i32, _dp, _i64]),
     "nfftk_get_params": (_i32, [_i32, _i64p, _i32]),
     "nfftk_get_sizes": (_i32, [_i32, _i32p, _i32p, _i32p, _i32]),
     "nfftk_get_window": (_i32, [_i32, _dp, _dp, _i32]),

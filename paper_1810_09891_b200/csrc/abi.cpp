@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -26,15 +27,21 @@ using namespace nfftk;
 
 namespace {
 
+// One handle.  `mu` serialises every call on the handle: the reference
+// documents that a plan may be shared by concurrent callers (serialised by
+// the GIL there); here the transforms share per-plan device scratch (grid,
+// staging buffers, ticket counters, captured graphs), so a second thread on
+// the same handle waits instead of interleaving with the first.
 struct Entry {
   Plan* plan = nullptr;
   int err_code = 0;
   int err_kind = 0;
   std::string err_msg;
+  std::mutex mu;
 };
 
 std::mutex g_lock;
-std::unordered_map<int32_t, Entry*> g_registry;
+std::unordered_map<int32_t, std::shared_ptr<Entry>> g_registry;
 int32_t g_next_handle = 1;
 int64_t g_live_buffers = 0;
 thread_local int g_create_kind = 0;
@@ -42,11 +49,26 @@ thread_local std::string g_create_msg;
 const char* const ABI_VERSION = "0.1.0";
 const char* const EXT_VERSION = "b200-0.1.0";
 
-Entry* lookup(int32_t h) {
+std::shared_ptr<Entry> lookup_shared(int32_t h) {
   std::lock_guard<std::mutex> g(g_lock);
   auto it = g_registry.find(h);
   return it == g_registry.end() ? nullptr : it->second;
 }
+
+// A looked-up handle, locked for the duration of one ABI call.  Converts to
+// nullptr for an unknown (or concurrently destroyed) handle.
+class EntryLock {
+ public:
+  explicit EntryLock(int32_t h) : e_(lookup_shared(h)) {
+    if (e_) lk_ = std::unique_lock<std::mutex>(e_->mu);
+  }
+  operator Entry*() const { return e_ && e_->plan ? e_.get() : nullptr; }
+  Entry* operator->() const { return e_.get(); }
+
+ private:
+  std::shared_ptr<Entry> e_;
+  std::unique_lock<std::mutex> lk_;
+};
 
 int32_t store(Entry* e, int kind, const std::string& msg) {
   e->err_kind = kind;
@@ -84,7 +106,7 @@ int32_t do_create(const int32_t* bandlimits, int32_t rank, int32_t node_count,
   try {
     std::vector<int> N(bandlimits, bandlimits + rank);
     Plan* p = plan_create(N, node_count, n, m, f1, f2, window, single);
-    Entry* e = new Entry();
+    auto e = std::make_shared<Entry>();
     e->plan = p;
     std::lock_guard<std::mutex> g(g_lock);
     int32_t h = g_next_handle++;
@@ -185,7 +207,7 @@ int32_t nfftk_create_advanced(const int32_t* bandlimits, int32_t rank, int32_t n
 }
 
 int32_t nfftk_set_x(int32_t h, const double* coords, int64_t len) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   if (len < 0) return ERR_SHAPE;  // abi.py:179-182 (no stored message)
   return guarded(e, [&] {
@@ -195,7 +217,7 @@ int32_t nfftk_set_x(int32_t h, const double* coords, int64_t len) {
 }
 
 static int32_t set_complex(int32_t h, const double* values, int64_t len, bool fhat) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   if (len < 0) return ERR_SHAPE;
   return guarded(e, [&] {
@@ -218,42 +240,42 @@ int32_t nfftk_set_f(int32_t h, const double* values, int64_t len) {
 }
 
 int32_t nfftk_trafo(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { host_transform(e->plan, true); });
 }
 
 int32_t nfftk_adjoint(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { host_transform(e->plan, false); });
 }
 
 const double* nfftk_get_f(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return nullptr;
   try { return f_buf(e->plan); } catch (...) { return nullptr; }
 }
 
 const double* nfftk_get_fhat(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return nullptr;
   try { return fhat_buf(e->plan); } catch (...) { return nullptr; }
 }
 
 int32_t nfftk_last_error(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   return e ? e->err_code : ERR_HANDLE;
 }
 
 const char* nfftk_last_error_message(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return "invalid handle";
   return e->err_code ? e->err_msg.c_str() : "";
 }
 
 int32_t nfftk_destroy(int32_t h) {
-  Entry* e = nullptr;
+  std::shared_ptr<Entry> e;
   {
     std::lock_guard<std::mutex> g(g_lock);
     auto it = g_registry.find(h);
@@ -262,8 +284,10 @@ int32_t nfftk_destroy(int32_t h) {
     g_registry.erase(it);
     g_live_buffers -= 2;
   }
+  // waits for a call in flight on this handle; later lookups fail (-1)
+  std::lock_guard<std::mutex> g(e->mu);
   delete e->plan;
-  delete e;
+  e->plan = nullptr;
   return 0;
 }
 
@@ -290,24 +314,24 @@ int32_t nfftk_last_create_error_kind(void) { return g_create_kind; }
 const char* nfftk_last_create_error_message(void) { return g_create_msg.c_str(); }
 
 int32_t nfftk_last_error_kind(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   return e ? e->err_kind : EK_HANDLE;
 }
 
 int32_t nfftk_set_nodes(int32_t h, const double* coords, int64_t len) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_set_nodes_host(e->plan, coords, len); });
 }
 
 int32_t nfftk_set_nodes_device(int32_t h, const double* coords, int64_t len, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_set_nodes_device(e->plan, coords, len, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_precompute(int32_t h) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] {
     Plan* p = e->plan;
@@ -316,80 +340,98 @@ int32_t nfftk_precompute(int32_t h) {
 }
 
 int32_t nfftk_precompute_stream(int32_t h, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_precompute(e->plan, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_trafo_host(int32_t h, const void* fhat, void* f) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_trafo_host(e->plan, fhat, f); });
 }
 
 int32_t nfftk_adjoint_host(int32_t h, const void* f, void* fhat) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_adjoint_host(e->plan, f, fhat); });
 }
 
 int32_t nfftk_ndft_host(int32_t h, const double* fhat, double* f) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_ndft_host(e->plan, fhat, f, false); });
 }
 
 int32_t nfftk_ndft_adjoint_host(int32_t h, const double* f, double* fhat) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_ndft_host(e->plan, f, fhat, true); });
 }
 
 int32_t nfftk_ndft_device(int32_t h, const void* fhat, void* f, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_ndft_device(e->plan, fhat, f, false, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_ndft_adjoint_device(int32_t h, const void* f, void* fhat, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_ndft_device(e->plan, f, fhat, true, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_trafo_device(int32_t h, const void* fhat, void* f, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_trafo_device(e->plan, fhat, f, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_adjoint_device(int32_t h, const void* f, void* fhat, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_adjoint_device(e->plan, f, fhat, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_spread_device(int32_t h, const void* f, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_spread_device(e->plan, f, (cudaStream_t)stream); });
 }
 
+int32_t nfftk_interp_device(int32_t h, void* f, void* stream) {
+  EntryLock e(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] { plan_interp_device(e->plan, f, (cudaStream_t)stream); });
+}
+
+int32_t nfftk_deconv_cols(int32_t h, int32_t dim, double* out, int64_t len) {
+  EntryLock e(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] {
+    Plan* p = e->plan;
+    if (dim < 0 || dim >= p->d) fail(EK_SHAPE, "dimension index outside the plan");
+    std::vector<double> c = plan_deconv_cols(p, dim);
+    if (len != (int64_t)c.size()) fail(EK_SHAPE, "deconvolution column needs N_i entries");
+    memcpy(out, c.data(), sizeof(double) * c.size());
+  });
+}
+
 int32_t nfftk_adjoint_finish_device(int32_t h, void* fhat, void* stream) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_adjoint_finish_device(e->plan, fhat, (cudaStream_t)stream); });
 }
 
 int32_t nfftk_bind_grid(int32_t h, void* dev, int64_t bytes) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_bind_grid(e->plan, dev, bytes); });
 }
 
 // params: [d, M, m, window, precision, f1, f2, has_nodes, ready, mode, ntiles, nsubs, width_sum]
 int32_t nfftk_get_params(int32_t h, int64_t* out, int32_t count) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   Plan* p = e->plan;
   int64_t v[13] = {p->d, p->M, p->m, p->window, p->single ? 1 : 0, (int64_t)p->f1, (int64_t)p->f2,
@@ -399,7 +441,7 @@ int32_t nfftk_get_params(int32_t h, int64_t* out, int32_t count) {
 }
 
 int32_t nfftk_get_sizes(int32_t h, int32_t* N, int32_t* n, int32_t* T, int32_t count) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   Plan* p = e->plan;
   for (int i = 0; i < count && i < p->d; ++i) {
@@ -411,7 +453,7 @@ int32_t nfftk_get_sizes(int32_t h, int32_t* N, int32_t* n, int32_t* T, int32_t c
 }
 
 int32_t nfftk_get_window(int32_t h, double* b, double* sigma, int32_t count) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   Plan* p = e->plan;
   for (int i = 0; i < count && i < p->d; ++i) {
@@ -422,7 +464,7 @@ int32_t nfftk_get_window(int32_t h, double* b, double* sigma, int32_t count) {
 }
 
 int32_t nfftk_phi_hut(int32_t h, int32_t dim, double* out, int64_t len) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] {
     Plan* p = e->plan;
@@ -434,7 +476,7 @@ int32_t nfftk_phi_hut(int32_t h, int32_t dim, double* out, int64_t len) {
 }
 
 int32_t nfftk_node_order(int32_t h, int64_t* out, int64_t len) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] {
     if (len != e->plan->M) fail(EK_SHAPE, "node order needs M entries");
@@ -443,7 +485,7 @@ int32_t nfftk_node_order(int32_t h, int64_t* out, int64_t len) {
 }
 
 int32_t nfftk_window_evals(int32_t h, int64_t* last, int64_t* total) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   if (last) *last = e->plan->window_evals_last;
   if (total) *total = e->plan->window_evals_total;
@@ -451,7 +493,7 @@ int32_t nfftk_window_evals(int32_t h, int64_t* last, int64_t* total) {
 }
 
 int32_t nfftk_set_psi_policy(int32_t h, int32_t mode) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   if (mode < -1 || mode > MODE_TENSOR) return ERR_DOMAIN;
   e->plan->psi_policy = mode;
@@ -459,14 +501,14 @@ int32_t nfftk_set_psi_policy(int32_t h, int32_t mode) {
 }
 
 int32_t nfftk_set_timing(int32_t h, int32_t on) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   e->plan->timing = on != 0;
   return 0;
 }
 
 int32_t nfftk_phase_times(int32_t h, double* ms, int64_t* calls, int32_t count, int32_t reset) {
-  Entry* e = lookup(h);
+  EntryLock e(h);
   if (!e) return ERR_HANDLE;
   return guarded(e, [&] { plan_phase_times(e->plan, ms, calls, count, reset); });
 }

@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -17,10 +18,11 @@
 
 namespace nfftk {
 
-static unsigned long long g_launches = 0;  // kernels launched by this library
-unsigned long long launch_count() { return g_launches; }
-void count_launch() { ++g_launches; }
-void add_launches(unsigned long long n) { g_launches += n; }
+// kernels launched by this library (any thread, any handle: atomic)
+static std::atomic<unsigned long long> g_launches{0};
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // cells per segment when a line of len cells is cut into nseg warp-sized pieces
 __host__ __device__ inline int seg_width(int len, int nseg) {

@@ -426,20 +426,25 @@ void plan_set_nodes_host(Plan* p, const double* x, int64_t len) {
   ++p->gen;
   shape_check_x(p, len);
   check_range_host(p, x);
-  std::vector<double> copy(x, x + p->M * p->d);
   if (p->d <= MAX_D) {
+    // straight from the caller's buffer (the call blocks until the copy is
+    // done); no host copy is kept -- the device holds the nodes
     ensure_stream(p);
     if (!p->x_dev) NFFTK_CUDA(cudaMalloc(&p->x_dev, sizeof(double) * p->M * p->d));
-    NFFTK_CUDA(cudaMemcpyAsync(p->x_dev, copy.data(), sizeof(double) * p->M * p->d,
+    NFFTK_CUDA(cudaMemcpyAsync(p->x_dev, x, sizeof(double) * p->M * p->d,
                                cudaMemcpyHostToDevice, p->own_stream));
     invalidate_tables(p);
     p->has_nodes = false;
+    p->x_host.clear();
+    p->x_host.shrink_to_fit();
     nodes_to_device(p, p->own_stream);
     NFFTK_CUDA(cudaStreamSynchronize(p->own_stream));
   } else {
+    // d > 3 has no fast transform; the exact sums read the host copy
+    std::vector<double> copy(x, x + p->M * p->d);
     invalidate_tables(p);
+    p->x_host.swap(copy);
   }
-  p->x_host.swap(copy);
   p->has_nodes = true;
 }
 
@@ -550,8 +555,8 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   // the device always keeps them (their cost is negligible).
   std::vector<double> cols;
   for (int i = 0; i < p->d; ++i) {
-    std::vector<double> t = plan_phi_hut(p, i);
-    for (int k = 0; k < p->N[i]; ++k) cols.push_back(1.0 / (t[k] * p->wscale[i]));
+    std::vector<double> c = plan_deconv_cols(p, i);
+    cols.insert(cols.end(), c.begin(), c.end());
   }
   if (!p->cols) NFFTK_CUDA(cudaMalloc(&p->cols, sizeof(double) * cols.size()));
   NFFTK_CUDA(cudaMemcpyAsync(p->cols, cols.data(), sizeof(double) * cols.size(),
@@ -649,16 +654,34 @@ static void exec_fft(Plan* p, int dir, cudaStream_t s) {
   if (r != CUFFT_SUCCESS) fail(EK_CUDA, "cufftExec failed (" + std::to_string((int)r) + ")");
 }
 
-void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
+// B alone (kernels.py:122-197): samples at the plan's nodes from the dense
+// n-grid already in p->grid (the multi-GPU trafo fills a bound grid with a
+// distributed F first).
+void plan_interp_device(Plan* p, void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
-  { PhaseScope ps(p, PH_DECONV, s); launch_deconv(p->single, fhat, p->grid, p->dq, s); }
-  { PhaseScope ps(p, PH_FFT_FWD, s); exec_fft(p, CUFFT_FORWARD, s); }
   { PhaseScope ps(p, PH_PAD, s); launch_pad(p->single, p->grid, p->gp, p->pq, s); }
   { PhaseScope ps(p, PH_INTERP, s);
     launch_interp(p->single, p->tmap, p->gp, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
+}
+
+void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
+  require_ready(p);
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  { PhaseScope ps(p, PH_DECONV, s); launch_deconv(p->single, fhat, p->grid, p->dq, s); }
+  { PhaseScope ps(p, PH_FFT_FWD, s); exec_fft(p, CUFFT_FORWARD, s); }
+  plan_interp_device(p, f, s);
+}
+
+// Deconvolution column of dim i as the kernels apply it: 1 / (phi_hat_i(k)
+// * wscale_i) for k = -N_i/2 .. N_i/2 - 1 (transform.py:44-54; wscale is the
+// complex64 window normalisation, 1 for complex128).
+std::vector<double> plan_deconv_cols(const Plan* p, int dim) {
+  std::vector<double> t = plan_phi_hut(p, dim), out;
+  for (int k = 0; k < p->N[dim]; ++k) out.push_back(1.0 / (t[k] * p->wscale[dim]));
+  return out;
 }
 
 void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
@@ -743,6 +766,7 @@ static void host_call(Plan* p, int dir, const void* in, void* out, Body body) {
   }
   const bool usable = !p->graphs_off && !p->timing && !getenv("NFFTK_NO_HOST_GRAPH") &&
                       is_pinned(in) && is_pinned(out);
+  bool captured_now = false;
   if (usable && !h.exec && h.seen >= 1) {
     const unsigned long long l0 = launch_count();
     cudaGraph_t graph = nullptr;
@@ -766,13 +790,14 @@ static void host_call(Plan* p, int dir, const void* in, void* out, Body body) {
       h.exec = exec;
       h.launches = launch_count() - l0;
       add_launches(0ull - h.launches);  // the capture itself launched nothing
+      captured_now = true;              // ... but body() already counted this call's evals
     }
   }
   ++h.seen;
   if (usable && h.exec) {
     NFFTK_CUDA(cudaGraphLaunch(h.exec, s));
     add_launches(h.launches);
-    count_evals(p);  // the host-side counter update the captured call made once
+    if (!captured_now) count_evals(p);  // the host-side update a replay skips
   } else {
     body(s);
   }

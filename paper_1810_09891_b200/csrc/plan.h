@@ -114,6 +114,8 @@ void plan_precompute(Plan* p, cudaStream_t s);
 void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s);
 void plan_adjoint_device(Plan* p, const void* f, void* fhat, cudaStream_t s);
 void plan_spread_device(Plan* p, const void* f, cudaStream_t s);
+void plan_interp_device(Plan* p, void* f, cudaStream_t s);
+std::vector<double> plan_deconv_cols(const Plan* p, int dim);
 void plan_adjoint_finish_device(Plan* p, void* fhat, cudaStream_t s);
 void plan_trafo_host(Plan* p, const void* fhat, void* f);
 void plan_adjoint_host(Plan* p, const void* f, void* fhat);

@@ -352,6 +352,30 @@ class Plan:
         want = torch.complex64 if self.single else torch.complex128
         return t.reshape(length).to(want).contiguous()
 
+    def _check_out_array(self, out, length, what):
+        """``out=`` for the host path: the library writes ``length`` elements
+        of the plan's complex type at ``out.ctypes.data``."""
+        if not isinstance(out, np.ndarray):
+            raise ShapeError(f"{what} out= must be a numpy array on the host path")
+        if out.dtype != self.cdtype or out.size != length or not out.flags.c_contiguous \
+                or not out.flags.writeable:
+            raise ShapeError(f"{what} out= must be a writeable C-contiguous {np.dtype(self.cdtype).name} "
+                             f"array of {length} entries, got {out.dtype} shape {out.shape}")
+        return out
+
+    def _check_out_tensor(self, out, length, what, device):
+        """``out=`` for the device path: a contiguous tensor of the plan's
+        complex dtype on the input's device."""
+        import torch
+
+        want = torch.complex64 if self.single else torch.complex128
+        if not (_is_torch(out) and out.is_cuda):
+            raise ShapeError(f"{what} out= must be a CUDA tensor on the device path")
+        if out.dtype != want or out.numel() != length or not out.is_contiguous() or out.device != device:
+            raise ShapeError(f"{what} out= must be a contiguous {want} tensor of {length} entries on "
+                             f"{device}, got {out.dtype} shape {tuple(out.shape)} on {out.device}")
+        return out
+
     def trafo(self, fhat, out=None):
         """f = B F D f_hat at the M nodes (transform.py:92-118)."""
         lib = self._lib_checked()
@@ -362,12 +386,14 @@ class Plan:
             fhat = self._as_tensor(fhat, self.num_freqs, "fhat")
             if out is None:
                 out = torch.empty(self.M, dtype=fhat.dtype, device=fhat.device)
+            self._check_out_tensor(out, self.M, "trafo", fhat.device)
             self._check(lib.nfftk_trafo_device(self._h, ctypes.c_void_p(fhat.data_ptr()),
                                                ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
             return out
         fhat = self._as_vector(fhat, self.num_freqs, "fhat")
         if out is None:
             out = np.empty(self.M, dtype=self.cdtype)
+        self._check_out_array(out, self.M, "trafo")
         self._check(lib.nfftk_trafo_host(self._h, fhat.ctypes.data, out.ctypes.data))
         return out
 
@@ -381,30 +407,66 @@ class Plan:
             f = self._as_tensor(f, self.M, "f")
             if out is None:
                 out = torch.empty(self.num_freqs, dtype=f.dtype, device=f.device)
+            self._check_out_tensor(out, self.num_freqs, "adjoint", f.device)
             self._check(lib.nfftk_adjoint_device(self._h, ctypes.c_void_p(f.data_ptr()),
                                                  ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
             return out
         f = self._as_vector(f, self.M, "f")
         if out is None:
             out = np.empty(self.num_freqs, dtype=self.cdtype)
+        self._check_out_array(out, self.num_freqs, "adjoint")
         self._check(lib.nfftk_adjoint_host(self._h, f.ctypes.data, out.ctypes.data))
         return out
 
     # -- multi-GPU building blocks (distributed.py) -----------------------
     def spread(self, f):
         """B^H only, into the plan grid (device tensor input)."""
+        if not (_is_torch(f) and f.is_cuda):
+            raise ShapeError("spread() takes a CUDA tensor")
         f = self._as_tensor(f, self.M, "f")
         self._check(self._lib_checked().nfftk_spread_device(
             self._h, ctypes.c_void_p(f.data_ptr()), _stream_ptr()))
 
+    def interp(self, out=None):
+        """B alone: samples at the plan's nodes from its dense grid (a grid
+        bound with ``bind_grid`` and filled by the caller -- the slab trafo of
+        distributed.py), on the current stream."""
+        import torch
+
+        lib = self._lib_checked()
+        self._require_ready()
+        grid = getattr(self, "_bound_grid", None)
+        if grid is None:
+            raise PlanStateError("interp() reads a bound grid; call bind_grid() first")
+        if out is None:
+            out = torch.empty(self.M, dtype=torch.complex64 if self.single else torch.complex128,
+                              device=grid.device)
+        self._check_out_tensor(out, self.M, "interp", grid.device)
+        self._check(lib.nfftk_interp_device(self._h, ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
+        return out
+
+    def deconv_cols(self, i):
+        """1 / (phi_hat_i(k) * wscale_i) for k = -N_i/2 .. N_i/2 - 1: the
+        deconvolution column D applies with 1/|I_n| (transform.py:44-63)."""
+        out = np.empty(self.N[i])
+        self._check(self._lib_checked().nfftk_deconv_cols(
+            self._h, int(i), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size))
+        return out
+
     def adjoint_finish(self, out):
         """F^H and D^H of the (already reduced) plan grid into ``out``."""
+        import torch
+
+        self._check_out_tensor(out, self.num_freqs, "adjoint_finish",
+                               out.device if _is_torch(out) else torch.device("cuda"))
         self._check(self._lib_checked().nfftk_adjoint_finish_device(
             self._h, ctypes.c_void_p(out.data_ptr()), _stream_ptr()))
         return out
 
     def bind_grid(self, tensor):
         """Use a caller-owned device tensor as the plan's oversampled grid."""
+        if not (_is_torch(tensor) and tensor.is_cuda and tensor.is_contiguous()):
+            raise ShapeError("bind_grid() takes a contiguous CUDA tensor")
         nbytes = tensor.numel() * tensor.element_size()
         self._check(self._lib_checked().nfftk_bind_grid(self._h, ctypes.c_void_p(tensor.data_ptr()),
                                                         nbytes))

@@ -5,7 +5,10 @@ Run here (the reference exists only in this container, never on the GPU box):
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py
 
-Outputs (committed): ``tests/golden/*.npz``.  Inputs are regenerated from the
+Outputs (committed): ``tests/golden/*.npz``.  ``make_golden.py C3 C4 C5`` runs
+the reference at those configurations' full sizes (C5: ~6 min, ~33 GB RSS on
+8 cores) and writes ``<C>_full.npz``: 65,536 seeded entries of trafo and of
+adjoint plus whole-vector norms, sums and 4,096 block sums.  Inputs are regenerated from the
 seeds in ``paper_1810_09891_b200/workloads.py`` and stored alongside for the
 small cases, so the fixtures are self-contained.
 """
@@ -83,22 +86,39 @@ def small_cases():
     return cases
 
 
-def config_case(name, full):
+def config_case(name, full, sub=4096):
+    """One BASELINE configuration at its FULL size through the reference Plan
+    (default flags, all reference threads).  ``full`` stores both output
+    vectors; otherwise ``sub`` seeded entries of each plus whole-vector norms,
+    sums and a checksum of per-block sums (so a GPU run at full size is
+    compared entry-wise on the subsample and vector-wide through the sums)."""
     w = wl.CONFIGS[name]
     x = wl.nodes(w)
     fh = wl.fhat(w)
     fs = wl.samples(w)
     out_f, out_fhat, _, _ = run_case(w.N, w.n, w.m, x, fh, fs)
     rec = dict(norm_f=np.linalg.norm(out_f), norm_fhat=np.linalg.norm(out_fhat),
-               sum_f=out_f.sum(), sum_fhat=out_fhat.sum())
+               sum_f=out_f.sum(), sum_fhat=out_fhat.sum(),
+               blocksum_f=block_sums(out_f), blocksum_fhat=block_sums(out_fhat))
     if full:
         rec.update(trafo=out_f, adjoint=out_fhat)
     else:
         sel = np.random.default_rng(11)
-        jf = np.sort(sel.choice(w.M, 4096, replace=False))
-        jk = np.sort(sel.choice(w.num_freqs, 4096, replace=False))
-        rec.update(trafo_idx=jf, trafo_sub=out_f[jf], adjoint_idx=jk, adjoint_sub=out_fhat[jk])
+        jf = np.sort(sel.choice(w.M, min(sub, w.M), replace=False))
+        jk = np.sort(sel.choice(w.num_freqs, min(sub, w.num_freqs), replace=False))
+        rec.update(trafo_idx=jf.astype(np.int64), trafo_sub=out_f[jf],
+                   adjoint_idx=jk.astype(np.int64), adjoint_sub=out_fhat[jk])
     return rec
+
+
+BLOCKS = 4096
+
+
+def block_sums(v, blocks=BLOCKS):
+    """Sums of ``blocks`` contiguous equal slices (the last absorbs the rest):
+    a size-independent whole-vector check that localises a wrong region."""
+    edges = (np.arange(blocks + 1, dtype=np.int64) * v.size) // blocks
+    return np.add.reduceat(v, edges[:-1])
 
 
 def pins():
@@ -137,6 +157,14 @@ def pins():
 
 
 def main():
+    big = [a for a in sys.argv[1:] if a in ("C3", "C4", "C5")]
+    if big:
+        # full-size goldens for the large configs: 65,536 entries of each output
+        for name in big:
+            rec = config_case(name, False, sub=65536)
+            np.savez_compressed(os.path.join(HERE, f"{name}_full.npz"), **rec)
+            print(name, "full-size golden done", flush=True)
+        return
     os.makedirs(HERE, exist_ok=True)
     threads = nfftk.get_threads()
     print("reference threads:", threads)
