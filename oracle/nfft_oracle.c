@@ -227,20 +227,29 @@ void oracle_fft_nd(int d, const int *n, cplx *data, int sign) {
         int64_t outer = total / (len * inner);
         fft_plan1d p = make_plan1d(len, sign);
         int64_t lines = outer * inner;
+        /* lines along a strided axis are moved in blocks of LB neighbours
+         * (LB contiguous elements per step instead of one): the same 1-D
+         * transforms, cache-friendly gathers */
+        int64_t LB = 16;
+        while (inner % LB) LB /= 2;
+        const int64_t blocks = outer * (inner / LB);
+        (void)lines;
 #pragma omp parallel
         {
             int64_t sl = p.pow2 ? len : p.L;
-            cplx *line = (cplx *)malloc(sizeof(cplx) * (size_t)len);
+            cplx *buf = (cplx *)malloc(sizeof(cplx) * (size_t)(len * LB));
             cplx *scr = (cplx *)malloc(sizeof(cplx) * (size_t)sl);
 #pragma omp for schedule(static)
-            for (int64_t li = 0; li < lines; ++li) {
-                int64_t o = li / inner, in = li % inner;
-                cplx *base = data + o * len * inner + in;
-                for (int64_t k = 0; k < len; ++k) line[k] = base[k * inner];
-                fft_line(&p, line, scr);
-                for (int64_t k = 0; k < len; ++k) base[k * inner] = line[k];
+            for (int64_t bi = 0; bi < blocks; ++bi) {
+                int64_t o = bi / (inner / LB), in0 = (bi % (inner / LB)) * LB;
+                cplx *base = data + o * len * inner + in0;
+                for (int64_t k = 0; k < len; ++k)
+                    for (int64_t u = 0; u < LB; ++u) buf[u * len + k] = base[k * inner + u];
+                for (int64_t u = 0; u < LB; ++u) fft_line(&p, buf + u * len, scr);
+                for (int64_t k = 0; k < len; ++k)
+                    for (int64_t u = 0; u < LB; ++u) base[k * inner + u] = buf[u * len + k];
             }
-            free(line);
+            free(buf);
             free(scr);
         }
         free_plan1d(&p);
@@ -276,25 +285,25 @@ static int setup(oplan *p, int d, const int *N, const int *n, int m, int code, i
     return 0;
 }
 
-/* kernels.py:42-53 -- wrapped cells + factors for node j, dim i */
-static int dim_factors(const oplan *p, const double *x, int64_t j, int i, int64_t *wrap, double *fac) {
+/* kernels.py:42-53 -- the factors of node j, dim i at cells lo .. lo+w-1 */
+static int dim_factors(const oplan *p, const double *x, int64_t j, int i, int64_t *lo_out, double *fac) {
     double n_i = (double)p->n[i];
     double y = x[j * p->d + i] * n_i;
     int64_t lo = (int64_t)ceil(y - p->m);
     int w = (int)((int64_t)floor(y + p->m) - lo + 1);
     for (int t = 0; t < w; ++t) {
         int64_t cell = lo + t;
-        wrap[t] = floor_mod(cell, p->n[i]);
         double off = x[j * p->d + i] - (double)cell / n_i;
         if (p->mode == MODE_LUT)
             fac[t] = lut_factor(p->lut + i * (LUT_SIZE + 1), LUT_SIZE, p->lut_step[i], off);
         else
             fac[t] = oracle_window_factor(p->code, off, n_i, (double)p->m, p->b[i]);
     }
+    *lo_out = lo;
     return w;
 }
 
-/* transform.py:44-63 -- per-dim factors over k = -N/2..N/2-1 */
+/* transform.py:44-54 -- per-dim factors over k = -N/2..N/2-1 */
 static double **deconv_cols(const oplan *p) {
     double **cols = (double **)malloc(sizeof(double *) * p->d);
     for (int i = 0; i < p->d; ++i) {
@@ -343,210 +352,382 @@ static int64_t freq_slot(const oplan *p, int64_t lin, int *kk) {
     return slot;
 }
 
-int oracle_gather_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
-                       const double *x, const cplx *g, cplx *f);
+/* ------------------------------------------------------ lexicographic order */
 
-/* transform.py:92-118 -- f = B F D f_hat */
-int oracle_trafo(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
-                 const double *x, const cplx *fhat, cplx *f) {
-    oplan p;
-    if (setup(&p, d, N, n, m, code, mode)) return -1;
-    int64_t G = grid_total(&p), K = freq_total(&p);
-    cplx *g = (cplx *)calloc((size_t)G, sizeof(cplx));
-    double **cols = deconv_cols(&p);
-    double gs = (double)G;
-    for (int64_t lin = 0; lin < K; ++lin) {
-        int kk[3];
-        int64_t slot = freq_slot(&p, lin, kk);
-        g[slot] = deconv_value(&p, cols, fhat[lin], kk, gs);
+/* Stable LSD radix sort of (key, idx) pairs, 8-bit digits, OpenMP histograms.
+ * Ties keep index order, so sorting (key, 0..M-1) reproduces np.lexsort. */
+static void sort_pairs(uint64_t *key, int64_t *idx, int64_t M, int bits) {
+    uint64_t *k2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(M > 0 ? M : 1));
+    int64_t *i2 = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M > 0 ? M : 1));
+    int nt = 1;
+#ifdef _OPENMP
+    nt = omp_get_max_threads();
+#endif
+    int64_t *hist = (int64_t *)malloc(sizeof(int64_t) * 256 * (size_t)nt);
+    for (int shift = 0; shift < bits; shift += 8) {
+        memset(hist, 0, sizeof(int64_t) * 256 * (size_t)nt);
+#pragma omp parallel num_threads(nt)
+        {
+            int t = 0;
+#ifdef _OPENMP
+            t = omp_get_thread_num();
+#endif
+            int64_t lo = M * t / nt, hi = M * (t + 1) / nt;
+            int64_t *h = hist + 256 * t;
+            for (int64_t q = lo; q < hi; ++q) h[(key[q] >> shift) & 255]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                int64_t run = 0;
+                for (int digit = 0; digit < 256; ++digit)
+                    for (int u = 0; u < nt; ++u) {
+                        int64_t c = hist[256 * u + digit];
+                        hist[256 * u + digit] = run;
+                        run += c;
+                    }
+            }
+            for (int64_t q = lo; q < hi; ++q) {
+                int64_t pos = h[(key[q] >> shift) & 255]++;
+                k2[pos] = key[q];
+                i2[pos] = idx[q];
+            }
+        }
+        memcpy(key, k2, sizeof(uint64_t) * (size_t)M);
+        memcpy(idx, i2, sizeof(int64_t) * (size_t)M);
     }
-    free_cols(&p, cols);
-    oracle_fft_nd(d, n, g, -1);
-    oracle_gather_grid(d, N, n, m, code, mode, M, x, g, f);
-    free(g);
-    free(p.lut);
-    return 0;
+    free(hist);
+    free(k2);
+    free(i2);
 }
 
-/* kernels.py:122-197 -- B alone: f_j from a given (FFT'd) oversampled grid;
- * prange over nodes, lexicographic accumulation */
-int oracle_gather_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
-                       const double *x, const cplx *g, cplx *f) {
-    oplan p;
-    if (setup(&p, d, N, n, m, code, mode)) return -1;
+/* plan.py:228-231 -- lexsort of floor(n x), dim 0 primary, stable */
+void oracle_node_order(int d, const int *n, int64_t M, const double *x, int64_t *order) {
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(M > 0 ? M : 1));
+    uint64_t space = 1;
+    for (int i = 0; i < d; ++i) space *= (uint64_t)(n[i] + 1);
 #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < M; ++j) {
-        int64_t w0[64], w1[64], w2[64];
-        double f0[64], f1[64], f2[64];
+        uint64_t k = 0;
+        for (int i = 0; i < d; ++i)
+            k = k * (uint64_t)(n[i] + 1) + (uint64_t)((int64_t)floor(x[j * d + i] * (double)n[i]) + n[i] / 2);
+        key[j] = k;
+        order[j] = j;
+    }
+    int bits = 1;
+    while (bits < 64 && ((uint64_t)1 << bits) < space) ++bits;
+    sort_pairs(key, order, M, bits);
+    free(key);
+}
+
+/* ------------------------------------------------------------------ plan */
+
+/* The reference plan's node state and tables (plan.py:202-299): stencil
+ * starts and widths (node_ranges, indexing.py:114-124), the lexicographic
+ * node order (NFFT_SORT_NODES), and the factor table psi (M, d, 2m+1) --
+ * PRE_PSI, kernels.py:56-72; in LUT mode the table holds the interpolated
+ * factors, the values kernels.py:30-39 forms per use.  Building them is the
+ * reference's set_nodes + precompute; trafo / adjoint then only read them, as
+ * the reference's transforms do under its default flags. */
+typedef struct {
+    oplan p;
+    int64_t M;
+    int K;
+    double *x;        /* (M, d) */
+    int64_t *lo;      /* (M, d) */
+    int *width;       /* (M, d) */
+    double *psi;      /* (M, d, K) */
+    int64_t *order;   /* lexicographic order */
+    char *wraps;      /* per sorted position: dim-0 rows wrap (transform.py:144-158) */
+} oracle_plan;
+
+void oracle_plan_destroy(void *h) {
+    oracle_plan *q = (oracle_plan *)h;
+    if (!q) return;
+    free(q->x); free(q->lo); free(q->width); free(q->psi); free(q->order); free(q->wraps);
+    free(q->p.lut);
+    free(q);
+}
+
+void *oracle_plan_create(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                         const double *x) {
+    oracle_plan *q = (oracle_plan *)calloc(1, sizeof(oracle_plan));
+    if (!q || setup(&q->p, d, N, n, m, code, mode)) { free(q); return NULL; }
+    q->M = M;
+    q->K = 2 * m + 1;
+    size_t nd = (size_t)(M > 0 ? M : 1) * d;
+    q->x = (double *)malloc(sizeof(double) * nd);
+    q->lo = (int64_t *)malloc(sizeof(int64_t) * nd);
+    q->width = (int *)malloc(sizeof(int) * nd);
+    q->psi = (double *)malloc(sizeof(double) * nd * q->K);
+    q->order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M > 0 ? M : 1));
+    q->wraps = (char *)malloc((size_t)(M > 0 ? M : 1));
+    if (!q->x || !q->lo || !q->width || !q->psi || !q->order || !q->wraps) {
+        oracle_plan_destroy(q);
+        return NULL;
+    }
+    memcpy(q->x, x, sizeof(double) * (size_t)M * d);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < M; ++j)
+        for (int i = 0; i < d; ++i) {
+            double *row = q->psi + ((size_t)j * d + i) * q->K;
+            int64_t lo;
+            int w = dim_factors(&q->p, q->x, j, i, &lo, row);
+            for (int t = w; t < q->K; ++t) row[t] = 0.0;
+            q->lo[(size_t)j * d + i] = lo;
+            q->width[(size_t)j * d + i] = w;
+        }
+    oracle_node_order(d, n, M, q->x, q->order);
+    for (int64_t oi = 0; oi < M; ++oi) {
+        size_t j = (size_t)q->order[oi] * d;
+        q->wraps[oi] = floor_mod(q->lo[j], n[0]) + q->width[j] > n[0];
+    }
+    return q;
+}
+
+/* Software prefetch of the grid rows node j's stencil reads (d >= 2): the
+ * natural-order gather of the reference touches a fresh, random part of the
+ * grid per node, so the port issues the next nodes' row loads ahead (the
+ * arithmetic and its order are unchanged). */
+#define GATHER_AHEAD 4
+static inline void prefetch_rows(const oracle_plan *q, const cplx *g, int64_t j) {
+    if (j >= q->M) return;
+    const int d = q->p.d;
+    const int64_t n0 = q->p.n[0], n1 = q->p.n[1], n2 = q->p.n[2];
+    const int64_t *lo = q->lo + (size_t)j * d;
+    const int *W = q->width + (size_t)j * d;
+    if (d == 2) {
+        int64_t c1 = floor_mod(lo[1], n1);
+        for (int t0 = 0; t0 < W[0]; ++t0) {
+            const cplx *r = g + floor_mod(lo[0] + t0, n0) * n1 + c1;
+            __builtin_prefetch(r);
+            __builtin_prefetch(r + W[1] - 1);
+        }
+    } else if (d == 3) {
+        int64_t c2 = floor_mod(lo[2], n2);
+        for (int t0 = 0; t0 < W[0]; ++t0) {
+            int64_t b0 = floor_mod(lo[0] + t0, n0) * n1;
+            for (int t1 = 0; t1 < W[1]; ++t1) {
+                const cplx *r = g + (b0 + floor_mod(lo[1] + t1, n1)) * n2 + c2;
+                __builtin_prefetch(r);
+                __builtin_prefetch(r + W[2] - 1);
+            }
+        }
+    }
+}
+
+/* kernels.py:122-197 -- B: prange over nodes in natural order, lexicographic
+ * accumulation ((p0 * f1) * f2) * g */
+int oracle_plan_gather_grid(void *h, const cplx *g, cplx *f) {
+    const oracle_plan *q = (const oracle_plan *)h;
+    const int d = q->p.d, K = q->K;
+    const int64_t n0 = q->p.n[0], n1 = q->p.n[1], n2 = q->p.n[2];
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < q->M; ++j) {
+        prefetch_rows(q, g, j + GATHER_AHEAD);
+        const double *f0 = q->psi + (size_t)j * d * K;
+        const int64_t *lo = q->lo + (size_t)j * d;
+        const int *W = q->width + (size_t)j * d;
         cplx acc = 0.0;
-        int W0 = dim_factors(&p, x, j, 0, w0, f0);
         if (d == 1) {
-            for (int t0 = 0; t0 < W0; ++t0) acc += f0[t0] * g[w0[t0]];
+            for (int t0 = 0; t0 < W[0]; ++t0) acc += f0[t0] * g[floor_mod(lo[0] + t0, n0)];
         } else if (d == 2) {
-            int W1 = dim_factors(&p, x, j, 1, w1, f1);
-            for (int t0 = 0; t0 < W0; ++t0) {
-                int64_t base = w0[t0] * n[1];
+            const double *f1 = f0 + K;
+            int64_t w1[64];
+            for (int t1 = 0; t1 < W[1]; ++t1) w1[t1] = floor_mod(lo[1] + t1, n1);
+            for (int t0 = 0; t0 < W[0]; ++t0) {
+                int64_t base = floor_mod(lo[0] + t0, n0) * n1;
                 double p0 = f0[t0];
-                for (int t1 = 0; t1 < W1; ++t1) acc += (p0 * f1[t1]) * g[base + w1[t1]];
+                for (int t1 = 0; t1 < W[1]; ++t1) acc += (p0 * f1[t1]) * g[base + w1[t1]];
             }
         } else {
-            int W1 = dim_factors(&p, x, j, 1, w1, f1);
-            int W2 = dim_factors(&p, x, j, 2, w2, f2);
-            for (int t0 = 0; t0 < W0; ++t0) {
-                int64_t base0 = w0[t0] * n[1];
+            const double *f1 = f0 + K, *f2 = f0 + 2 * K;
+            int64_t w1[64], w2[64];
+            for (int t1 = 0; t1 < W[1]; ++t1) w1[t1] = floor_mod(lo[1] + t1, n1);
+            for (int t2 = 0; t2 < W[2]; ++t2) w2[t2] = floor_mod(lo[2] + t2, n2);
+            for (int t0 = 0; t0 < W[0]; ++t0) {
+                int64_t base0 = floor_mod(lo[0] + t0, n0) * n1;
                 double p0 = f0[t0];
-                for (int t1 = 0; t1 < W1; ++t1) {
-                    int64_t base1 = (base0 + w1[t1]) * n[2];
+                for (int t1 = 0; t1 < W[1]; ++t1) {
+                    int64_t base1 = (base0 + w1[t1]) * n2;
                     double p01 = p0 * f1[t1];
-                    for (int t2 = 0; t2 < W2; ++t2) acc += (p01 * f2[t2]) * g[base1 + w2[t2]];
+                    for (int t2 = 0; t2 < W[2]; ++t2) acc += (p01 * f2[t2]) * g[base1 + w2[t2]];
                 }
             }
         }
         f[j] = acc;
     }
-    free(p.lut);
     return 0;
 }
 
-/* kernels.py:209-281 -- spread one node (all rows, or rows [t_begin, t_end) of dim 0) */
-static void spread_node(const oplan *p, const double *x, int64_t j, cplx fj, cplx *g,
+/* transform.py:92-118 -- f = B F D f_hat */
+int oracle_plan_trafo(void *h, const cplx *fhat, cplx *f) {
+    const oracle_plan *q = (const oracle_plan *)h;
+    const oplan *p = &q->p;
+    int64_t G = grid_total(p), K = freq_total(p);
+    cplx *g = (cplx *)calloc((size_t)G, sizeof(cplx));
+    if (!g) return -2;
+    double **cols = deconv_cols(p);
+    double gs = (double)G;
+#pragma omp parallel for schedule(static)
+    for (int64_t lin = 0; lin < K; ++lin) {
+        int kk[3];
+        int64_t slot = freq_slot(p, lin, kk);
+        g[slot] = deconv_value(p, cols, fhat[lin], kk, gs);
+    }
+    free_cols(p, cols);
+    oracle_fft_nd(p->d, p->n, g, -1);
+    oracle_plan_gather_grid(h, g, f);
+    free(g);
+    return 0;
+}
+
+/* kernels.py:209-281 -- spread one node (all rows, or rows [s_lo, s_hi) of dim 0) */
+static void spread_node(const oracle_plan *q, int64_t j, cplx fj, cplx *g,
                         int restrict_rows, int64_t s_lo, int64_t s_hi) {
-    int64_t w0[64], w1[64], w2[64];
-    double f0[64], f1[64], f2[64];
-    int d = p->d;
-    int W0 = dim_factors(p, x, j, 0, w0, f0);
-    int t_begin = 0, t_end = W0;
+    const int d = q->p.d, K = q->K;
+    const int64_t n0 = q->p.n[0], n1 = q->p.n[1], n2 = q->p.n[2];
+    const double *f0 = q->psi + (size_t)j * d * K;
+    const int64_t *lo = q->lo + (size_t)j * d;
+    const int *W = q->width + (size_t)j * d;
+    int t_begin = 0, t_end = W[0];
     if (restrict_rows) {
         /* kernels.py:304-312 -- slab-owned rows of a non-wrapping node */
-        int64_t a0 = w0[0];
+        int64_t a0 = floor_mod(lo[0], n0);
         t_begin = s_lo > a0 ? (int)(s_lo - a0) : 0;
-        int64_t row_end = a0 + W0 < s_hi ? a0 + W0 : s_hi;
+        int64_t row_end = a0 + W[0] < s_hi ? a0 + W[0] : s_hi;
         t_end = (int)(row_end - a0);
         if (t_begin >= t_end) return;
     }
     if (d == 1) {
-        for (int t0 = t_begin; t0 < t_end; ++t0) g[w0[t0]] += fj * f0[t0];
+        for (int t0 = t_begin; t0 < t_end; ++t0) g[floor_mod(lo[0] + t0, n0)] += fj * f0[t0];
         return;
     }
-    int W1 = dim_factors(p, x, j, 1, w1, f1);
+    const double *f1 = f0 + K;
+    int64_t w1[64];
+    for (int t1 = 0; t1 < W[1]; ++t1) w1[t1] = floor_mod(lo[1] + t1, n1);
     if (d == 2) {
         for (int t0 = t_begin; t0 < t_end; ++t0) {
-            int64_t base = w0[t0] * p->n[1];
+            int64_t base = floor_mod(lo[0] + t0, n0) * n1;
             double p0 = f0[t0];
-            for (int t1 = 0; t1 < W1; ++t1) g[base + w1[t1]] += fj * (p0 * f1[t1]);
+            for (int t1 = 0; t1 < W[1]; ++t1) g[base + w1[t1]] += fj * (p0 * f1[t1]);
         }
         return;
     }
-    int W2 = dim_factors(p, x, j, 2, w2, f2);
+    const double *f2 = f0 + 2 * K;
+    int64_t w2[64];
+    for (int t2 = 0; t2 < W[2]; ++t2) w2[t2] = floor_mod(lo[2] + t2, n2);
     for (int t0 = t_begin; t0 < t_end; ++t0) {
-        int64_t base0 = w0[t0] * p->n[1];
+        int64_t base0 = floor_mod(lo[0] + t0, n0) * n1;
         double p0 = f0[t0];
-        for (int t1 = 0; t1 < W1; ++t1) {
-            int64_t base1 = (base0 + w1[t1]) * p->n[2];
+        for (int t1 = 0; t1 < W[1]; ++t1) {
+            int64_t base1 = (base0 + w1[t1]) * n2;
             double p01 = p0 * f1[t1];
-            for (int t2 = 0; t2 < W2; ++t2) g[base1 + w2[t2]] += fj * (p01 * f2[t2]);
+            for (int t2 = 0; t2 < W[2]; ++t2) g[base1 + w2[t2]] += fj * (p01 * f2[t2]);
         }
     }
-}
-
-typedef struct { int64_t key[3]; int64_t idx; } sort_rec;
-static int g_sort_d;
-static int cmp_rec(const void *a, const void *b) {
-    const sort_rec *ra = (const sort_rec *)a, *rb = (const sort_rec *)b;
-    for (int i = 0; i < g_sort_d; ++i) {
-        if (ra->key[i] < rb->key[i]) return -1;
-        if (ra->key[i] > rb->key[i]) return 1;
-    }
-    return ra->idx < rb->idx ? -1 : (ra->idx > rb->idx);
-}
-
-/* plan.py:228-231 -- lexsort of floor(n x), dim 0 primary, stable */
-void oracle_node_order(int d, const int *n, int64_t M, const double *x, int64_t *order) {
-    sort_rec *r = (sort_rec *)malloc(sizeof(sort_rec) * (size_t)M);
-    for (int64_t j = 0; j < M; ++j) {
-        for (int i = 0; i < d; ++i) r[j].key[i] = (int64_t)floor(x[j * d + i] * (double)n[i]);
-        r[j].idx = j;
-    }
-    g_sort_d = d;
-    qsort(r, (size_t)M, sizeof(sort_rec), cmp_rec);
-    for (int64_t j = 0; j < M; ++j) order[j] = r[j].idx;
-    free(r);
 }
 
 /* transform.py:121-171 -- B^H only: the oversampled grid after spreading
  * (before the FFT).  blockwise != 0 restates the slab-owned parallel adjoint
- * (kernels.py:293-401, transform.py:144-158); otherwise the sequential
- * natural-order spread (transform.py:159-171).  nthreads <= 0 uses the
- * OpenMP default. */
-int oracle_spread_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
-                       const double *x, const cplx *f, cplx *g, int blockwise, int nthreads) {
-    oplan p;
-    if (setup(&p, d, N, n, m, code, mode)) return -1;
+ * (kernels.py:293-401, transform.py:144-158): slab s owns dim-0 rows
+ * [n0 s/P, n0 (s+1)/P), every slab walks all sorted nodes, nodes whose rows
+ * wrap go to a sequential epilogue; otherwise the sequential natural-order
+ * spread (transform.py:159-171).  nthreads <= 0 uses the OpenMP default. */
+int oracle_plan_spread_grid(void *h, const cplx *f, cplx *g, int blockwise, int nthreads) {
+    const oracle_plan *q = (const oracle_plan *)h;
 #ifdef _OPENMP
     if (nthreads <= 0) nthreads = omp_get_max_threads();
 #else
     nthreads = 1;
 #endif
-    int64_t G = grid_total(&p);
+    int64_t G = grid_total(&q->p);
     memset(g, 0, sizeof(cplx) * (size_t)G);
+    const int64_t M = q->M;
     if (blockwise && nthreads > 1) {
-        int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)M);
-        oracle_node_order(d, n, M, x, order);
-        int64_t n0 = n[0];
-        char *wraps = (char *)malloc((size_t)M);
-        for (int64_t oi = 0; oi < M; ++oi) {
-            double y = x[order[oi] * d] * (double)n0;
-            int64_t lo = (int64_t)ceil(y - m);
-            int64_t W0 = (int64_t)floor(y + m) - lo + 1;
-            wraps[oi] = floor_mod(lo, n0) + W0 > n0;
-        }
+        int64_t n0 = q->p.n[0];
 #pragma omp parallel for num_threads(nthreads) schedule(static, 1)
         for (int s = 0; s < nthreads; ++s) {
             int64_t s_lo = (n0 * s) / nthreads, s_hi = (n0 * (s + 1)) / nthreads;
             for (int64_t oi = 0; oi < M; ++oi) {
-                if (wraps[oi]) continue;
-                spread_node(&p, x, order[oi], f[order[oi]], g, 1, s_lo, s_hi);
+                if (q->wraps[oi]) continue;
+                spread_node(q, q->order[oi], f[q->order[oi]], g, 1, s_lo, s_hi);
             }
         }
-        /* sequential epilogue for nodes whose leading rows wrap */
         for (int64_t oi = 0; oi < M; ++oi)
-            if (wraps[oi]) spread_node(&p, x, order[oi], f[order[oi]], g, 0, 0, 0);
-        free(wraps);
-        free(order);
+            if (q->wraps[oi]) spread_node(q, q->order[oi], f[q->order[oi]], g, 0, 0, 0);
     } else {
-        for (int64_t j = 0; j < M; ++j) spread_node(&p, x, j, f[j], g, 0, 0, 0);
+        for (int64_t j = 0; j < M; ++j) spread_node(q, j, f[j], g, 0, 0, 0);
     }
-    free(p.lut);
     return 0;
 }
 
 /* transform.py:174-176 -- F^H (sign +1) and D^H of a spread grid (in place) */
-int oracle_adjoint_finish(int d, const int *N, const int *n, int m, int code, cplx *g, cplx *fhat) {
-    oplan p;
-    if (setup(&p, d, N, n, m, code, MODE_DIRECT)) return -1;
-    int64_t G = grid_total(&p), K = freq_total(&p);
-    oracle_fft_nd(d, n, g, +1);
-    double **cols = deconv_cols(&p);
+static int adjoint_finish_p(const oplan *p, cplx *g, cplx *fhat) {
+    int64_t G = grid_total(p), K = freq_total(p);
+    oracle_fft_nd(p->d, p->n, g, +1);
+    double **cols = deconv_cols(p);
     double gs = (double)G;
+#pragma omp parallel for schedule(static)
     for (int64_t lin = 0; lin < K; ++lin) {
         int kk[3];
-        int64_t slot = freq_slot(&p, lin, kk);
-        fhat[lin] = deconv_value(&p, cols, g[slot], kk, gs);
+        int64_t slot = freq_slot(p, lin, kk);
+        fhat[lin] = deconv_value(p, cols, g[slot], kk, gs);
     }
-    free_cols(&p, cols);
+    free_cols(p, cols);
     return 0;
 }
 
+int oracle_adjoint_finish(int d, const int *N, const int *n, int m, int code, cplx *g, cplx *fhat) {
+    oplan p;
+    if (setup(&p, d, N, n, m, code, MODE_DIRECT)) return -1;
+    return adjoint_finish_p(&p, g, fhat);
+}
+
 /* transform.py:121-176 -- f_hat = D^H F^H B^H f */
+int oracle_plan_adjoint(void *h, const cplx *f, cplx *fhat, int blockwise, int nthreads) {
+    const oracle_plan *q = (const oracle_plan *)h;
+    cplx *g = (cplx *)malloc(sizeof(cplx) * (size_t)grid_total(&q->p));
+    if (!g) return -2;
+    oracle_plan_spread_grid(h, f, g, blockwise, nthreads);
+    int rc = adjoint_finish_p(&q->p, g, fhat);
+    free(g);
+    return rc;
+}
+
+/* one-shot forms: plan, transform, release */
+int oracle_trafo(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                 const double *x, const cplx *fhat, cplx *f) {
+    void *h = oracle_plan_create(d, N, n, m, code, mode, M, x);
+    if (!h) return -1;
+    int rc = oracle_plan_trafo(h, fhat, f);
+    oracle_plan_destroy(h);
+    return rc;
+}
+
+int oracle_gather_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                       const double *x, const cplx *g, cplx *f) {
+    void *h = oracle_plan_create(d, N, n, m, code, mode, M, x);
+    if (!h) return -1;
+    int rc = oracle_plan_gather_grid(h, g, f);
+    oracle_plan_destroy(h);
+    return rc;
+}
+
+int oracle_spread_grid(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
+                       const double *x, const cplx *f, cplx *g, int blockwise, int nthreads) {
+    void *h = oracle_plan_create(d, N, n, m, code, mode, M, x);
+    if (!h) return -1;
+    int rc = oracle_plan_spread_grid(h, f, g, blockwise, nthreads);
+    oracle_plan_destroy(h);
+    return rc;
+}
+
 int oracle_adjoint(int d, const int *N, const int *n, int m, int code, int mode, int64_t M,
                    const double *x, const cplx *f, cplx *fhat, int blockwise, int nthreads) {
-    if (d < 1 || d > 3) return -1;
-    int64_t G = 1;
-    for (int i = 0; i < d; ++i) G *= n[i];
-    cplx *g = (cplx *)malloc(sizeof(cplx) * (size_t)G);
-    int rc = oracle_spread_grid(d, N, n, m, code, mode, M, x, f, g, blockwise, nthreads);
-    if (!rc) rc = oracle_adjoint_finish(d, N, n, m, code, g, fhat);
-    free(g);
+    void *h = oracle_plan_create(d, N, n, m, code, mode, M, x);
+    if (!h) return -1;
+    int rc = oracle_plan_adjoint(h, f, fhat, blockwise, nthreads);
+    oracle_plan_destroy(h);
     return rc;
 }
 

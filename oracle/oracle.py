@@ -44,6 +44,13 @@ def lib():
         L.oracle_spread_grid.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int,
                                          ctypes.c_int]
+        L.oracle_plan_create.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int64, vp]
+        L.oracle_plan_create.restype = vp
+        L.oracle_plan_destroy.argtypes = [vp]
+        L.oracle_plan_destroy.restype = None
+        L.oracle_plan_trafo.argtypes = [vp, vp, vp]
+        L.oracle_plan_adjoint.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int]
         L.oracle_gather_grid.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int64, vp, vp, vp]
         L.oracle_adjoint_finish.argtypes = [ctypes.c_int, i32p, i32p, ctypes.c_int, ctypes.c_int,
@@ -81,6 +88,47 @@ def _ptr(a):
 
 def _kind(window):
     return GAUSSIAN if str(window).lower() == "gaussian" else KAISER_BESSEL
+
+
+class Plan:
+    """The reference plan's node state and tables (plan.py:202-299: stencils,
+    lexicographic order, PRE_PSI factor table) built once; ``trafo`` /
+    ``adjoint`` then read them, as the reference's transforms do under its
+    default flags (the CPU baseline times only the transforms, like the
+    reference's time_mean10 protocol, metrics.py:59-67)."""
+
+    def __init__(self, N, n, m, x, window="kaiserbessel", lut=False):
+        self.x = np.ascontiguousarray(x, dtype=np.float64)
+        self.M, self.d = self.x.shape
+        self.N, self.n, self.m = tuple(int(v) for v in N), tuple(int(v) for v in n), int(m)
+        self._h = lib().oracle_plan_create(self.d, _ivec(N), _ivec(n), self.m, _kind(window),
+                                           MODE_LUT if lut else MODE_DIRECT, self.M, _ptr(self.x))
+        if not self._h:
+            raise MemoryError("oracle_plan_create failed (d <= 3, host memory)")
+
+    def trafo(self, fhat, out=None):
+        fhat = np.ascontiguousarray(fhat, dtype=np.complex128).ravel()
+        out = np.empty(self.M, dtype=np.complex128) if out is None else out
+        if lib().oracle_plan_trafo(self._h, _ptr(fhat), _ptr(out)):
+            raise MemoryError("oracle_plan_trafo failed")
+        return out
+
+    def adjoint(self, f, out=None, blockwise=None, threads=0):
+        if blockwise is None:
+            blockwise = self.d > 1
+        f = np.ascontiguousarray(f, dtype=np.complex128).ravel()
+        out = np.empty(int(np.prod(self.N)), dtype=np.complex128) if out is None else out
+        if lib().oracle_plan_adjoint(self._h, _ptr(f), _ptr(out), int(bool(blockwise)), int(threads)):
+            raise MemoryError("oracle_plan_adjoint failed")
+        return out
+
+    def close(self):
+        if self._h:
+            lib().oracle_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def trafo(N, n, m, x, fhat, window="kaiserbessel", lut=False):
