@@ -118,7 +118,7 @@ struct Geom {
   double lut_step[MAX_D];
   const double* psi;      // M * psi_row(d, 2m+1) in sorted order (MODE_TENSOR)
   const int4* rec;        // M per-node stencil records, sorted order
-  int psi_pad;            // PRE_PSI rows halo-indexed (pipelined kernels) vs stencil-indexed
+  int psi_pad;            // d = 3 pipelined PRE_PSI layout: 0 none (stencil rows), 1 halo-indexed, 2 sten3 blocks
   int pr;                 // PRE_PSI row stride (doubles)
   int64_t M;
   int nt_interp;          // threads per interp CTA
@@ -217,14 +217,41 @@ __device__ __forceinline__ double dim_factor(const Geom& g, int dim, double x, i
 // for bulk copies and 128-bit shared loads.
 __host__ __device__ inline int psi_row(int d, int K) { return (d * K + 1) & ~1; }
 
-// Halo-indexed PRE_PSI row (pipelined kernels): every leading dim i as a row
-// of the tile halo's H_i cells (zero off the stencil, so a halo row reads its
-// factor without a stencil test), then the 2m+1 last-dim factors; even count.
+// Halo-indexed PRE_PSI row (Geom::psi_pad = 1): every leading dim i as a row
+// of the tile halo's H_i cells (zero off the stencil, so a halo row reads
+// its factor with no stencil test), then the 2m+1 last-dim factors; even
+// count.
 __host__ __device__ inline int psi_row_halo(int d, const int* H, int K) {
   int s = K;
   for (int i = 0; i + 1 < d; ++i) s += H[i];
   return (s + 1) & ~1;
 }
+
+// PRE_PSI row of the d = 3 pipelined kernels (Geom::psi_pad): three blocks of
+// K + 1 = 2m + 2 factors -- last dim, dim 0, dim 1 -- each the 2m+1 stencil
+// factors of kernels.py:56-72 (zero past the width) plus one zero, so a
+// kernel reads dim i's factor for halo cell h of a node whose stencil starts
+// at halo cell s as block_i[min((unsigned)(h - s), K)]: off-stencil cells
+// land on the zero without a branch.  The last-dim block comes first so its
+// factor pairs are 16-byte aligned.  3(K+1) factors per node (m = 4: 240
+// bytes) instead of the 2H+K+1 of halo-indexed rows (352 bytes).
+// Which layout the d = 3 pipelined kernels use: sten3 for complex128 plans
+// with m <= 4 (the run-window spread, C5: 352 -> 240 bytes per node, spread
+// and gather time unchanged), halo-indexed rows otherwise -- their spread
+// paths index without the stencil-start arithmetic (measured: C3 spread
+// 0.319 vs 0.351 ms, C5 c64 spread 20.0 vs 23.1 ms with halo rows).
+// Geom::psi_pad = 1 (halo-indexed) or 2 (sten3); NFFTK_HALO_ROWS forces 1.
+__host__ __device__ constexpr bool pipe_sten3(bool single, int m) {
+#ifdef NFFTK_HALO_ROWS
+  return false && single && m;
+#else
+  return !single && m <= 4;
+#endif
+}
+constexpr int STEN3_OW2 = 0;
+__host__ __device__ constexpr int sten3_ow0(int K) { return K + 1; }
+__host__ __device__ constexpr int sten3_ow1(int K) { return 2 * (K + 1); }
+__host__ __device__ constexpr int sten3_count(int K) { return 3 * (K + 1); }
 
 // PRE_PSI row stride in elements of the factor type: 16-byte rows (fp64
 // factors for c128 plans, fp32 factors for c64 plans on the pipelined

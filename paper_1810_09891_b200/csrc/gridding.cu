@@ -658,7 +658,13 @@ struct IPipeCfg {
   // factor type: fp64 rows for c128, fp32 rows for c64 (k_build_psi<float>),
   // each row padded to 16 bytes
   using W = R;
-  static constexpr int PR = psi_row_pad<W>(D == 3 ? H0 + H1 + K : 2 * K);
+  // d = 3: sten3 blocks or halo-indexed rows [H0 | H1 | 2m+1] (common.cuh
+  // pipe_sten3, the layout the plan built); d = 2: stencil rows [2m+1 | 2m+1]
+  static constexpr bool STEN3 = D == 3 && pipe_sten3(sizeof(R) == 4, MM);
+  static constexpr bool HALO_IDX = D == 3 && !STEN3;  // leading-dim factors at their halo cell
+  static constexpr int PR = psi_row_pad<W>(D == 2 ? 2 * K : (STEN3 ? sten3_count(K) : H0 + H1 + K));
+  static constexpr int OW0 = STEN3 ? sten3_ow0(K) : 0, OW1 = STEN3 ? sten3_ow1(K) : (D == 3 ? H0 : 0),
+                       OWL = STEN3 ? STEN3_OW2 : (D == 3 ? H0 + H1 : K);
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
   static constexpr size_t W_BYTES = al(sizeof(W) * NB * PR);
   static constexpr size_t R_BYTES = al(16 * (size_t)NB);
@@ -860,23 +866,26 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
         R are = 0, aim = 0;
         if (active) {
           const typename P::W* w = ws + jj * PR;
+          // factor blocks: leading dims at w + OW0 / OW1 (indexed from the
+          // node's stencil start o0 / o1 for halo-indexed rows, from 0
+          // otherwise), last dim at w + OWL
+          const int o0 = P::HALO_IDX ? q[0] : 0, o1 = P::HALO_IDX ? q[1] : 0;
           if constexpr (D == 3 && P::SCHED) {
             if (q[6])  // fast node: conflict-free row schedule
-              interp_node3_sched<MM, TEAM, H1, HS>(reinterpret_cast<const double2*>(halo), q, w,
-                                                   w + P::H0, w + P::H0 + P::H1, q[0], q[1], sch,
-                                                   are, aim);
+              interp_node3_sched<MM, TEAM, H1, HS>(reinterpret_cast<const double2*>(halo), q, w + P::OW0,
+                                                   w + P::OW1, w + P::OWL, o0, o1, sch, are, aim);
             else
-              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0],
-                                          q[1], tl, are, aim);
+              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w + P::OW0, w + P::OW1, w + P::OWL, o0, o1,
+                                          tl, are, aim);
           } else if constexpr (D == 3 && P::HALF) {
             if (q[6])  // fast node: half-row lanes on the conflict-free schedule
-              interp_node3_half<MM, H1, HS>(reinterpret_cast<const float2*>(halo), q, w, w + P::H0,
-                                            w + P::H0 + P::H1, q[0], q[1], tl & 1, sch, are, aim);
+              interp_node3_half<MM, H1, HS>(reinterpret_cast<const float2*>(halo), q, w + P::OW0,
+                                            w + P::OW1, w + P::OWL, o0, o1, tl & 1, sch, are, aim);
             else
-              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0],
-                                          q[1], tl, are, aim);
-          } else if constexpr (D == 3)  // halo-indexed rows [H0 | H1 | 2m+1]
-            interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w + P::H0, w + P::H0 + P::H1, q[0], q[1],
+              interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w + P::OW0, w + P::OW1, w + P::OWL, o0, o1,
+                                          tl, are, aim);
+          } else if constexpr (D == 3)
+            interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w + P::OW0, w + P::OW1, w + P::OWL, o0, o1,
                                         tl, are, aim);
           else  // stencil-indexed rows [2m+1 | 2m+1]
             interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w, w + K, 0, 0, tl, are, aim);
@@ -917,7 +926,7 @@ static Geom sched_geom(const Geom& g, int nsubs, int grid, int per_cta = 4) {
 }
 
 // Geometries the pipelined kernels (spread and interp) both cover; for d = 3
-// these get halo-indexed PRE_PSI tables (Geom::psi_pad).
+// these get the pipelined PRE_PSI layouts (Geom::psi_pad, common.cuh pipe_sten3).
 bool pipe_geometry(const Geom& g) {
   if (getenv("NFFTK_NO_PIPE")) return false;
   if (g.d == 3) return g.m >= 1 && g.m <= 6 && g.T[0] == 8 && g.T[1] == 8 && g.T[2] == 8;
@@ -926,7 +935,7 @@ bool pipe_geometry(const Geom& g) {
 }
 
 bool interp_pipe_ok(const Geom& g) {
-  return g.mode == MODE_TENSOR && g.psi && g.rec && pipe_geometry(g) && g.psi_pad == (g.d == 3);
+  return g.mode == MODE_TENSOR && g.psi && g.rec && pipe_geometry(g) && (g.psi_pad != 0) == (g.d == 3);
 }
 
 // Sorted copy of the samples for the spread: fs[i] = f[perm[i]].
@@ -1343,25 +1352,32 @@ struct PipeCfg {
   // at m = 6 (1 CTA/SM, 128 registers) and 3% faster for fp32 rows).
   static constexpr bool RUNACC = (BLOCKS == 2 || RPT > 1) && sizeof(R) == 8;
   using W = R;                                          // factor type (fp32 rows for c64)
-  static constexpr int PR = psi_row_pad<W>(2 * H + K);  // halo-indexed PRE_PSI row [H | H | 2m+1]
+  // PRE_PSI row: sten3 blocks [2m+2 | 2m+2 | 2m+2] or halo-indexed [H | H | 2m+1] (pipe_sten3)
+  static constexpr bool STEN3 = pipe_sten3(sizeof(R) == 4, MM);
+  static constexpr int PR = psi_row_pad<W>(STEN3 ? sten3_count(K) : 2 * H + K);
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
   static constexpr size_t stage_bytes(int nb) {
     return al(sizeof(W) * nb * PR) + al(16 * (size_t)nb) + al((size_t)ELEM * (nb + 2));
   }
-  static constexpr size_t rows_bytes = al((size_t)ROWS * HS * ELEM);
+  // staging rows: one per halo row (RUNACC: RPT per row group, GROUPS * RPT may exceed ROWS)
+  static constexpr size_t rows_bytes = al((size_t)(GROUPS * RPT > ROWS ? GROUPS * RPT : ROWS) * HS * ELEM);
   static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMeta) * s + 32); }
   static constexpr size_t total(int nb, int s) { return s * stage_bytes(nb) + ctl_bytes(s) + rows_bytes; }
   static constexpr size_t budget = BLOCKS == 2 ? 112 * 1024 : 224 * 1024;
+#ifndef NFFTK_SPREAD_MINS
+#define NFFTK_SPREAD_MINS 2
+#endif
+  // the largest batch whose ring is at least MINS deep, then the deepest ring
   static constexpr int pick_nb() {
     for (int nb : {32, 16, 8})
-      for (int s : {4, 3, 2})
-        if (total(nb, s) <= budget) return nb;
+      for (int s : {8, 6, 5, 4, 3, 2})
+        if (s >= NFFTK_SPREAD_MINS && total(nb, s) <= budget) return nb;
     return 0;
   }
   static constexpr int pick_s() {
     for (int nb : {32, 16, 8})
-      for (int s : {4, 3, 2})
-        if (total(nb, s) <= budget) return s;
+      for (int s : {8, 6, 5, 4, 3, 2})
+        if (s >= NFFTK_SPREAD_MINS && total(nb, s) <= budget) return s;
     return 0;
   }
   static constexpr int NB = pick_nb();
@@ -1385,6 +1401,22 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   constexpr int KP = (K + 1) / 2;
   constexpr int FA = 16 / (int)sizeof(C);  // samples per 16 bytes
   constexpr int NW = P::THREADS / 32;
+  // a node's factors for this thread's halo row (a, b): the leading-dim
+  // factors at halo cells a and b, and its K last-dim factors
+  // hs = the node's stencil starts (h0, h1) in halo cells, loaded one node
+  // ahead in the walks below (sten3 rows index the factors from them)
+  // sten3 rows: stencil offset (h - start) clamped onto the block's zero;
+  // halo-indexed rows: the factor at the halo cell itself
+  auto fa = [&](const typename P::W* w, int2 hs, int a) {
+    if constexpr (P::STEN3) return w[sten3_ow0(K) + min((unsigned)(a - hs.x), (unsigned)K)];
+    else return w[a];
+  };
+  auto fb = [&](const typename P::W* w, int2 hs, int b) {
+    if constexpr (P::STEN3) return w[sten3_ow1(K) + min((unsigned)(b - hs.y), (unsigned)K)];
+    else return w[H2 + b];
+  };
+  constexpr int OWL = P::STEN3 ? STEN3_OW2 : 2 * H2;
+  auto starts = [&](const int4* r) { return *reinterpret_cast<const int2*>(r); };
   extern __shared__ __align__(128) unsigned char smem[];
   // layout: ring stages | full[S] empty[S] meta[S] producer state | halo rows
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
@@ -1470,12 +1502,29 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   constexpr int RPT = P::RPT, HB = P::HB;
   const int grp = threadIdx.x;
   const bool gown = grp < P::GROUPS;  // padding threads own no row
-  const int a = gown ? grp / HB : 0, b0 = gown ? (grp % HB) * RPT : 0;
-  const int wa_lo = min((int)(threadIdx.x & ~31u), P::GROUPS - 1) / HB;
-  const int wa_hi = min((int)(threadIdx.x | 31u), P::GROUPS - 1) / HB;
-  C* const myrow = stage + (size_t)(a * H2 + b0) * HS;  // row j at myrow + j * HS
-  auto owns = [&](int j) { return gown && b0 + j < H2; };
+  // staging rows stay with the thread (its own bulk reductions guard them)
+  C* const myrow = stage + (size_t)(gown ? grp : 0) * RPT * HS;  // row j at myrow + j * HS
+#ifdef NFFTK_RUNACC_ALT
+  // alternating row maps (as in the whole-row path below): on odd tiles a
+  // thread holds row group (grp + GROUPS/2) mod GROUPS, so a warp that owns
+  // centre a-lines on one tile owns edge lines on the next
+  constexpr int SHG = P::GROUPS / 2;
+#else
+  constexpr int SHG = 0;
+#endif
+  int tpar = 0;
   for (;;) {  // tiles of this CTA
+    const int shift = tpar ? SHG : 0;
+    tpar ^= 1;
+    const int g2 = gown ? (grp + shift) % P::GROUPS : 0;
+    const int a = g2 / HB, b0 = (g2 % HB) * RPT;
+    auto owns = [&](int j) { return gown && b0 + j < H2; };
+    // this warp's a-lines: one interval, or two when its groups wrap
+    const int w0g = min((int)(threadIdx.x & ~31u), P::GROUPS - 1);
+    const int w1g = min((int)(threadIdx.x | 31u), P::GROUPS - 1);
+    const int s0g = (w0g + shift) % P::GROUPS, s1g = (w1g + shift) % P::GROUPS;
+    const int wa_lo = s0g / HB, wa_hi = s0g <= s1g ? s1g / HB : H2 - 1;
+    const int wb_lo = s0g <= s1g ? (1 << 20) : 0, wb_hi = s0g <= s1g ? -1 : s1g / HB;
     R accr[RPT][K], acci[RPT][K];
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
@@ -1549,17 +1598,19 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       const C* pf = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
       const int nb = (g.debug & 2) ? 0 : mt.nb;
       auto hits = [&](const int4 r) {
-        return (unsigned)r.z <= (unsigned)(H2 - K) && r.x <= wa_hi && r.x + (int)((unsigned)r.w & 0xffu) > wa_lo;
+        const int w0 = (int)((unsigned)r.w & 0xffu);
+        return (unsigned)r.z <= (unsigned)(H2 - K) &&
+               ((r.x <= wa_hi && r.x + w0 > wa_lo) || (r.x <= wb_hi && r.x + w0 > wb_lo));
       };
       // one node: coefficients f * w0[a] * w1[b0 + j] against the K last-dim factors
-      auto node1 = [&](const typename P::W* w, const C* fp) {
-        const typename P::W wa = w[a];
+      auto node1 = [&](const typename P::W* w, int2 hs, const C* fp) {
+        const typename P::W wa = fa(w, hs, a);
         R s[RPT];
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) s[j] = (R)(wa * w[H2 + b0 + j]);
+        for (int j = 0; j < RPT; ++j) s[j] = (R)(wa * fb(w, hs, b0 + j));
         run_touched = true;
         const C f = *fp;
-        const C* w2 = reinterpret_cast<const C*>(w + 2 * H2);
+        const C* w2 = reinterpret_cast<const C*>(w + OWL);
         C v[KP];
 #pragma unroll
         for (int p = 0; p < KP; ++p) v[p] = w2[p];
@@ -1590,11 +1641,18 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
         unsigned run = later ? mask & ((later & (0u - later)) - 1u) : mask;
         mask &= ~run;
         if (h != cur_h) move_window(h);
-        do {
-          const int jj = __ffs(run) - 1;
+        // the next node's stencil starts are loaded under this node's FMAs
+        int jj = __ffs(run) - 1;
+        int2 hs = starts(pr + jj);
+        for (;;) {
           run &= run - 1;
-          node1(pw + jj * PR, pf + jj);
-        } while (run);
+          const int jn = run ? __ffs(run) - 1 : jj;
+          const int2 hn = starts(pr + jn);
+          node1(pw + jj * PR, hs, pf + jj);
+          if (!run) break;
+          jj = jn;
+          hs = hn;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
@@ -1707,13 +1765,14 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
         touched = true;
 #define NFFTK_PIPE_NODE(H)                                                                 \
   {                                                                                        \
-    const int jj = __ffs(m2) - 1;                                                          \
     m2 &= m2 - 1;                                                                          \
+    const int jn = m2 ? __ffs(m2) - 1 : jj;                                                \
+    const int2 hn = starts(rs + jn); /* next node's starts, under this node's FMAs */      \
     const typename P::W* pw = ws + jj * PR;                                                \
-    const R s = (R)(pw[a] * pw[H2 + b]);                                                   \
+    const R s = (R)(fa(pw, hs, a) * fb(pw, hs, b));                                        \
     const C f = fv[jj];                                                                    \
     const R cr = f.x * s, ci = f.y * s;                                                    \
-    const C* w2 = reinterpret_cast<const C*>(pw + 2 * H2); /* factor pairs */             \
+    const C* w2 = reinterpret_cast<const C*>(pw + OWL); /* factor pairs */                 \
     _Pragma("unroll") for (int p = 0; p < KP; ++p) {                                       \
       const C v = w2[p];                                                                   \
       accr[H + 2 * p] = fma(cr, (R)v.x, accr[H + 2 * p]);                                  \
@@ -1723,11 +1782,15 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
         acci[H + 2 * p + 1] = fma(ci, (R)v.y, acci[H + 2 * p + 1]);                        \
       }                                                                                    \
     }                                                                                      \
+    jj = jn;                                                                               \
+    hs = hn;                                                                               \
   }
 #define NFFTK_PIPE_CASE(H)                                                     \
   case H:                                                                      \
     if constexpr (H + K <= H2) {                                               \
       unsigned m2 = run;                                                       \
+      int jj = __ffs(m2) - 1;                                                  \
+      int2 hs = starts(rs + jj);                                               \
       do {                                                                     \
         NFFTK_PIPE_NODE(H)                                                     \
       } while (m2);                                                            \
@@ -2075,6 +2138,7 @@ static void interp_go(const CUtensorMap* tm, const void* gp, void* f, void*, con
     if (interp_pipe_ok(g)) {
       using P = IPipeCfg<R, D, MM>;
       if (g.HS != P::HS) fail(EK_CUDA, "pipe interp: halo row stride mismatch");
+      if (D == 3 && g.psi_pad != (P::STEN3 ? 2 : 1)) fail(EK_CUDA, "pipe interp: PRE_PSI layout mismatch");
       auto kern = k_interp_pipe<R, D, MM>;
       NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
       static int sms = 0;
@@ -2122,6 +2186,7 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
         using P = PipeCfg<R, MM>;
         static_assert(P::NB > 0 && P::S >= 2, "pipe ring does not fit");
         if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
+        if (g.psi_pad != (P::STEN3 ? 2 : 1)) fail(EK_CUDA, "pipe spread: PRE_PSI layout mismatch");
         auto kern = k_spread_pipe<R, MM>;
         NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
         static int sms = 0;

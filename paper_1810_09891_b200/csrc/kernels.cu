@@ -133,10 +133,16 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
     int64_t i = q / pr;
     int r = (int)(q - i * pr);
     int dim = 0, t = r;
-    if (g.psi_pad) {
+    if (g.psi_pad == 1) {
       // halo-indexed leading dims, then the last dim's 2m+1 factors
       while (dim + 1 < g.d && t >= g.H[dim]) t -= g.H[dim++];
       if (dim + 1 == g.d && t >= K) dim = g.d;  // row padding
+    } else if (g.psi_pad == 2) {
+      // sten3 blocks of K + 1: last dim, dim 0, dim 1 (common.cuh)
+      const int blk = r / (K + 1);
+      t = r - blk * (K + 1);
+      dim = blk == 0 ? g.d - 1 : (blk == 1 ? 0 : (blk == 2 ? 1 : g.d));
+      if (t >= K) dim = g.d;  // the block's zero / row padding
     } else {
       dim = r / K;
       t = r - dim * K;
@@ -147,7 +153,7 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
     }
     double x = xs[dim * M + i];
     Stencil st = stencil(x, g.nd[dim], g.md);
-    if (g.psi_pad && dim + 1 < g.d) {
+    if (g.psi_pad == 1 && dim + 1 < g.d) {
       // halo cell t -> stencil offset t - h (h as in k_build_recs)
       int64_t slot = floor_mod(st.cell, g.n[dim]);
       int tcoord = (int)(slot / g.T[dim]);
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict
     const int dim = nd % g.d, j = nd / g.d;
     const Stencil st = stencil(xs[dim * M + i0 + j], g.nd[dim], g.md);
     int pos = dim * K;
-    if (g.psi_pad) {
+    if (g.psi_pad == 1) {
       // halo-indexed leading dims (stencil offset t at halo cell h + t), then
       // the last dim's 2m+1 factors -- k_build_psi's layout
       int off = 0;
@@ -199,6 +205,9 @@ __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict
         const int tcoord = (int)(slot / g.T[dim]);
         pos += (int)(slot - (int64_t)tcoord * g.T[dim]) + g.m - (int)(st.cell - st.lo);
       }
+    } else if (g.psi_pad == 2) {
+      // sten3 blocks: last dim, dim 0, dim 1 (common.cuh)
+      pos = dim == g.d - 1 ? STEN3_OW2 : (dim == 0 ? sten3_ow0(K) : sten3_ow1(K));
     }
     slo[nd] = st.lo;
     spos[nd] = pos;

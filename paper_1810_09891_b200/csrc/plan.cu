@@ -595,20 +595,16 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   p->geom.psi_f32 = 0;
   p->geom.pr = psi_row(p->d, 2 * p->m + 1);
   if (mode == MODE_TENSOR) {
-    p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? 1 : 0;
-    p->geom.pr = p->geom.psi_pad ? psi_row_halo(p->d, p->geom.H, 2 * p->m + 1)
-                                 : psi_row(p->d, 2 * p->m + 1);
+    const int K = 2 * p->m + 1;
+    p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? (pipe_sten3(p->single, p->m) ? 2 : 1) : 0;
+    const int pad_count = p->geom.psi_pad == 2 ? sten3_count(K) : psi_row_halo(p->d, p->geom.H, K);
+    p->geom.pr = p->geom.psi_pad ? psi_row_pad<double>(pad_count) : psi_row(p->d, K);
     // c64 plans on the pipelined geometries (only the pipelined kernels read
     // the table there) keep fp32 factor rows: half the bytes, no per-FMA
     // fp64 -> fp32 conversions
     if (p->single && pipe_geometry(p->geom)) {
       p->geom.psi_f32 = 1;
-      int s0 = 2 * p->m + 1;
-      if (p->geom.psi_pad)
-        for (int i = 0; i + 1 < p->d; ++i) s0 += p->geom.H[i];
-      else
-        s0 = p->d * (2 * p->m + 1);
-      p->geom.pr = psi_row_pad<float>(s0);
+      p->geom.pr = psi_row_pad<float>(p->geom.psi_pad ? pad_count : p->d * K);
     }
     const size_t esz = p->geom.psi_f32 ? sizeof(float) : sizeof(double);
     // psi_count counts doubles of storage
