@@ -167,6 +167,13 @@ int32_t nfftk_get_window(int32_t handle, double * b, double * sigma, int32_t cou
 int32_t nfftk_phi_hut(int32_t handle, int32_t dim, double * out, int64_t len);
 int32_t nfftk_node_order(int32_t handle, int64_t * out, int64_t len);
 int32_t nfftk_window_evals(int32_t handle, int64_t * last, int64_t * total);
+/* PrecomputeTables contents in the reference layout (plan.py:109-121), built
+ * on demand on the device and copied to host arrays: psi (M, d, 2m+1), len =
+ * M*d*(2m+1); vals / idx (M, (2m+1)^d) and counts (M) of PRE_FULL_PSI when
+ * vals is not NULL; lut (d, 2^14+1) and lut_steps (d) of PRE_LIN_PSI */
+int32_t nfftk_psi_tables(int32_t handle, double * psi, double * vals, int64_t * idx, int64_t * counts,
+                         int64_t len);
+int32_t nfftk_lut_tables(int32_t handle, double * lut, double * steps, int64_t len);
 
 /* instrumentation: per-phase CUDA-event timing and kernel launch counter */
 int32_t nfftk_set_timing(int32_t handle, int32_t on);
@@ -174,6 +181,17 @@ int32_t nfftk_phase_times(int32_t handle, double * ms, int64_t * calls, int32_t 
 uint64_t nfftk_launch_count(void);
 /* FP64 / FP32 FMA throughput of this GPU (TFLOP/s), for roofline reporting */
 int32_t nfftk_measure_fma_peaks(double * fp64_tflops, double * fp32_tflops);
+
+/* the library's window math (window.py:38-181) for host-side callers:
+ * shape parameter b_i, phi at offsets t, phi_hat at frequencies k (status
+ * per entry: 0 ok, 1 the Kaiser-Bessel transform vanishes, 2 not positive),
+ * the I0 series */
+double nfftk_window_b(int32_t window, int32_t N_i, int32_t n_i, int32_t m);
+int32_t nfftk_window_values(int32_t window, double n_i, int32_t m, double b_i, const double * t,
+                            int64_t count, double * out);
+int32_t nfftk_phi_hat_values(int32_t window, int32_t n_i, int32_t m, double b_i, const int32_t * k,
+                             int64_t count, double * out, int32_t * status);
+double nfftk_bessel_i0(double x);
 
 /* leak counters (cabi.py:240-245) */
 int32_t nfftk_live_handles(void);

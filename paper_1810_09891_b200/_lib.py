@@ -62,10 +62,16 @@ SIGNATURES = {
     "nfftk_phi_hut": (_i32, [_i32, _i32, _dp, _i64]),
     "nfftk_node_order": (_i32, [_i32, _i64p, _i64]),
     "nfftk_window_evals": (_i32, [_i32, _i64p, _i64p]),
+    "nfftk_psi_tables": (_i32, [_i32, _vp, _vp, _vp, _vp, _i64]),
+    "nfftk_lut_tables": (_i32, [_i32, _vp, _vp, _i64]),
     "nfftk_set_timing": (_i32, [_i32, _i32]),
     "nfftk_phase_times": (_i32, [_i32, _dp, _i64p, _i32, _i32]),
     "nfftk_launch_count": (_u64, []),
     "nfftk_measure_fma_peaks": (_i32, [_dp, _dp]),
+    "nfftk_window_b": (ctypes.c_double, [_i32, _i32, _i32, _i32]),
+    "nfftk_window_values": (_i32, [_i32, ctypes.c_double, _i32, ctypes.c_double, _vp, _i64, _vp]),
+    "nfftk_phi_hat_values": (_i32, [_i32, _i32, _i32, ctypes.c_double, _vp, _i64, _vp, _vp]),
+    "nfftk_bessel_i0": (ctypes.c_double, [ctypes.c_double]),
     "nfftk_live_handles": (_i32, []),
     "nfftk_live_buffers": (_i64, []),
 }

@@ -484,6 +484,25 @@ int32_t nfftk_node_order(int32_t h, int64_t* out, int64_t len) {
   });
 }
 
+int32_t nfftk_psi_tables(int32_t h, double* psi, double* vals, int64_t* idx, int64_t* counts, int64_t len) {
+  EntryLock e(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] {
+    Plan* p = e->plan;
+    if (len != p->M * p->d * (2 * p->m + 1)) fail(EK_SHAPE, "psi needs M * d * (2m+1) entries");
+    plan_psi_tables(p, psi, vals, idx, counts);
+  });
+}
+
+int32_t nfftk_lut_tables(int32_t h, double* lut, double* steps, int64_t len) {
+  EntryLock e(h);
+  if (!e) return ERR_HANDLE;
+  return guarded(e, [&] {
+    if (len != (int64_t)e->plan->d * (LUT_SIZE + 1)) fail(EK_SHAPE, "lut needs d * (2^14 + 1) entries");
+    plan_lut_tables(e->plan, lut, steps);
+  });
+}
+
 int32_t nfftk_window_evals(int32_t h, int64_t* last, int64_t* total) {
   EntryLock e(h);
   if (!e) return ERR_HANDLE;
@@ -514,6 +533,29 @@ int32_t nfftk_phase_times(int32_t h, double* ms, int64_t* calls, int32_t count, 
 }
 
 uint64_t nfftk_launch_count(void) { return launch_count(); }
+
+// ---- window math of the library for the host API (window.py:38-181): the
+// Python WindowModel evaluates through these, so the closed forms exist once
+double nfftk_window_b(int32_t window, int32_t N_i, int32_t n_i, int32_t m) {
+  return window_shape(window, N_i, n_i, m);
+}
+
+int32_t nfftk_window_values(int32_t window, double n_i, int32_t m, double b_i, const double* t,
+                            int64_t count, double* out) {
+  if (window != WINDOW_KB && window != WINDOW_GAUSS) return ERR_DOMAIN;
+  for (int64_t q = 0; q < count; ++q) out[q] = host_window(window, t[q], n_i, (double)m, b_i);
+  return 0;
+}
+
+// per entry: 0 ok, 1 KB transform vanishes, 2 not positive (out undefined then)
+int32_t nfftk_phi_hat_values(int32_t window, int32_t n_i, int32_t m, double b_i, const int32_t* k,
+                             int64_t count, double* out, int32_t* status) {
+  if (window != WINDOW_KB && window != WINDOW_GAUSS) return ERR_DOMAIN;
+  for (int64_t q = 0; q < count; ++q) status[q] = phi_hat_value(window, k[q], n_i, m, b_i, out + q);
+  return 0;
+}
+
+double nfftk_bessel_i0(double x) { return host_bessel_i0(x); }
 
 int32_t nfftk_measure_fma_peaks(double* fp64_tflops, double* fp32_tflops) {
   try {

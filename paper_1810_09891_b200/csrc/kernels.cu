@@ -275,6 +275,82 @@ void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, cudaStrea
   count_launch();
 }
 
+// PrecomputeTables.psi in the reference layout (plan.py:109-121, :258-266;
+// kernels.py:56-72): out[j, i, t] = window(x_ji - (lo_ji + t) / n_i) for t <
+// width, 0 beyond, natural node order, exact fp64 factors (no complex64
+// normalisation, no LUT).  Built on demand for callers that inspect it.
+__global__ void k_psi_reference(const double* __restrict__ x, int64_t M, Geom g, double* __restrict__ out) {
+  const int K = 2 * g.m + 1;
+  const int64_t total = M * g.d * K;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ji = q / K;
+    const int t = (int)(q - ji * K);
+    const int i = (int)(ji % g.d);
+    const double xv = x[ji];
+    const Stencil st = stencil(xv, g.nd[i], g.md);
+    double v = 0.0;
+    if (t < st.width) {
+      const double off = __dsub_rn(xv, (double)(st.lo + t) / g.nd[i]);
+      v = g.code == WINDOW_KB ? window_kb(off, g.nd[i], g.md, g.b[i]) : window_gauss(off, g.nd[i], g.b[i]);
+    }
+    out[q] = v;
+  }
+}
+
+// PRE_FULL_PSI tables in the reference layout (kernels.py:85-119): per node
+// the (2m+1)^d slots of products ((f0 f1) f2) over the stencil in
+// lexicographic order and their flat wrapped grid cells; slots past the
+// node's count stay zero (plan.py:270-279 zero-initialises both).
+__global__ void k_psi_full_reference(const double* __restrict__ psi, const double* __restrict__ x, int64_t M,
+                                     Geom g, double* __restrict__ vals, int64_t* __restrict__ idx,
+                                     int64_t* __restrict__ counts) {
+  const int K = 2 * g.m + 1;
+  int64_t P = 1;
+  for (int i = 0; i < g.d; ++i) P *= K;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo[MAX_D];
+    int W[MAX_D] = {1, 1, 1};
+    for (int i = 0; i < g.d; ++i) {
+      const Stencil st = stencil(x[j * g.d + i], g.nd[i], g.md);
+      lo[i] = st.lo;
+      W[i] = st.width;
+    }
+    const double* f = psi + j * g.d * K;
+    double* vo = vals + j * P;
+    int64_t* io = idx + j * P;
+    int64_t p = 0;
+    for (int t0 = 0; t0 < W[0]; ++t0) {
+      const int64_t r0 = floor_mod(lo[0] + t0, g.n[0]);
+      if (g.d == 1) { vo[p] = f[t0]; io[p++] = r0; continue; }
+      for (int t1 = 0; t1 < W[1]; ++t1) {
+        const int64_t r1 = floor_mod(lo[1] + t1, g.n[1]);
+        const double f01 = __dmul_rn(f[t0], f[K + t1]);
+        if (g.d == 2) { vo[p] = f01; io[p++] = r0 * g.n[1] + r1; continue; }
+        const int64_t r01 = (r0 * g.n[1] + r1) * g.n[2];
+        for (int t2 = 0; t2 < W[2]; ++t2) {
+          vo[p] = __dmul_rn(f01, f[2 * K + t2]);
+          io[p++] = r01 + floor_mod(lo[2] + t2, g.n[2]);
+        }
+      }
+    }
+    for (; p < P; ++p) { vo[p] = 0.0; io[p] = 0; }
+    int64_t c = 1;
+    for (int i = 0; i < g.d; ++i) c *= W[i];
+    counts[j] = c;
+  }
+}
+
+void psi_reference(const double* x_dev, int64_t M, const Geom& g, double* psi, double* vals, int64_t* idx,
+                   int64_t* counts, cudaStream_t s) {
+  k_psi_reference<<<blocks_for(M * g.d * (2 * g.m + 1), 256), 256, 0, s>>>(x_dev, M, g, psi);
+  count_launch();
+  if (vals) {
+    k_psi_full_reference<<<blocks_for(M, 128), 128, 0, s>>>(psi, x_dev, M, g, vals, idx, counts);
+    count_launch();
+  }
+}
+
 // Lexicographic cell order (plan.py:228-231): stable sort of (floor(n x)
 // row-major key, index) reproduces np.lexsort exactly.
 __global__ void k_lex_keys(const double* __restrict__ x, int64_t M, Geom g,

@@ -39,6 +39,8 @@ bool pipe_geometry(const Geom& g);
 bool spread_dense_ok(const Geom& g, int elem_bytes);
 void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, cudaStream_t s);
 void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaStream_t s);
+void psi_reference(const double* x_dev, int64_t M, const Geom& g, double* psi, double* vals, int64_t* idx,
+                   int64_t* counts, cudaStream_t s);
 
 void launch_deconv(bool single, const void* fhat, void* grid, const DeconvGeomH& q, cudaStream_t s);
 void launch_pack(bool single, const void* grid, void* fhat, const DeconvGeomH& q, cudaStream_t s);

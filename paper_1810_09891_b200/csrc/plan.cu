@@ -79,23 +79,37 @@ double host_window(int code, double t, double n_i, double m, double b_i) {
   return std::exp(-nt * nt / b_i) / std::sqrt(M_PI * b_i);
 }
 
-// window.py:142-164 (phi_hat), checked strictly positive
-static double host_phi_hat(const Plan* p, int dim, int k) {
-  int n_i = p->n[dim];
-  double b = p->b[dim];
+// window.py:142-164 (phi_hat).  Returns 0 and the value, or 1 (the KB
+// transform vanishes: b^2 < (2 pi k / n)^2) / 2 (value not positive).
+int phi_hat_value(int code, int k, int n_i, int m, double b, double* out) {
   double val;
-  if (p->window == WINDOW_KB) {
+  if (code == WINDOW_KB) {
     double c = 2.0 * M_PI * k / n_i;
     double arg = b * b - c * c;
-    if (arg < 0.0)
-      fail(EK_WINDOW, "kaiserbessel transform vanishes at k=" + std::to_string(k));
-    val = host_bessel_i0(p->m * std::sqrt(arg)) / n_i;
+    if (arg < 0.0) return 1;
+    val = host_bessel_i0(m * std::sqrt(arg)) / n_i;
   } else {
     double c = M_PI * k / n_i;
     val = std::exp(-b * c * c) / n_i;
   }
-  if (!(val > 0.0)) fail(EK_WINDOW, "window transform not positive at k=" + std::to_string(k));
-  return val;
+  *out = val;
+  return val > 0.0 ? 0 : 2;
+}
+
+// window.py:101-111: b from sigma = n_i / N_i
+double window_shape(int code, int N_i, int n_i, int m) {
+  const double s = (double)n_i / (double)N_i;
+  return code == WINDOW_KB ? M_PI * (2.0 - 1.0 / s) : 2.0 * s * m / ((2.0 * s - 1.0) * M_PI);
+}
+
+// checked strictly positive (WindowDegenerateError)
+static double host_phi_hat(const Plan* p, int dim, int k) {
+  double val = 0.0;
+  switch (phi_hat_value(p->window, k, p->n[dim], p->m, p->b[dim], &val)) {
+    case 1: fail(EK_WINDOW, "kaiserbessel transform vanishes at k=" + std::to_string(k));
+    case 2: fail(EK_WINDOW, "window transform not positive at k=" + std::to_string(k));
+    default: return val;
+  }
 }
 
 std::vector<double> plan_phi_hut(const Plan* p, int dim) {
@@ -304,8 +318,7 @@ Plan* plan_create(const std::vector<int>& N_in, int64_t M, const int* n_opt, con
       if (s <= 1.0) fail(EK_NFFT, "oversampling factor must exceed 1");
       if ((double)p->m / p->n[i] >= 0.5) fail(EK_NFFT, "window support m/n must be below 1/2");
       p->sigma.push_back(s);
-      p->b.push_back(window == WINDOW_KB ? M_PI * (2.0 - 1.0 / s)
-                                         : 2.0 * s * p->m / ((2.0 * s - 1.0) * M_PI));
+      p->b.push_back(window_shape(window, p->N[i], p->n[i], p->m));
       // complex64 keeps window products in range by normalising by phi(0)
       p->wscale.push_back(single ? 1.0 / host_window(window, 0.0, p->n[i], p->m, p->b[i]) : 1.0);
     }
@@ -828,6 +841,52 @@ void plan_node_order(Plan* p, int64_t* out) {
   NFFTK_CUDA(cudaStreamSynchronize(p->own_stream));
   cudaFree(order);
   for (int64_t i = 0; i < p->M; ++i) out[i] = tmp[i];
+}
+
+// PrecomputeTables.psi / psi_full_* (plan.py:109-121) in the reference
+// layout, natural node order, computed on the device and copied to the
+// caller's host arrays; vals / idx / counts may be null (psi only).
+void plan_psi_tables(Plan* p, double* psi, double* vals, int64_t* idx, int64_t* counts) {
+  if (!p->has_nodes) fail(EK_STATE, "plan has no nodes; call set_nodes() first");
+  if (p->d > MAX_D) fail(EK_NFFT, "full window tables support d <= 3, got d=" + std::to_string(p->d));
+  ensure_stream(p);
+  cudaStream_t s = p->own_stream;
+  const int K = 2 * p->m + 1;
+  int64_t P = 1;
+  for (int i = 0; i < p->d; ++i) P *= K;
+  const size_t npsi = (size_t)p->M * p->d * K, nfull = vals ? (size_t)p->M * P : 0;
+  double *dpsi = nullptr, *dvals = nullptr;
+  int64_t *didx = nullptr, *dcnt = nullptr;
+  NFFTK_CUDA(cudaMallocAsync(&dpsi, sizeof(double) * npsi, s));
+  if (vals) {
+    NFFTK_CUDA(cudaMallocAsync(&dvals, sizeof(double) * nfull, s));
+    NFFTK_CUDA(cudaMallocAsync(&didx, sizeof(int64_t) * nfull, s));
+    NFFTK_CUDA(cudaMallocAsync(&dcnt, sizeof(int64_t) * p->M, s));
+  }
+  Geom g = p->geom;
+  g.wscale[0] = g.wscale[1] = g.wscale[2] = 1.0;
+  psi_reference(p->x_dev, p->M, g, dpsi, dvals, didx, dcnt, s);
+  if (psi) NFFTK_CUDA(cudaMemcpyAsync(psi, dpsi, sizeof(double) * npsi, cudaMemcpyDeviceToHost, s));
+  if (vals) {
+    NFFTK_CUDA(cudaMemcpyAsync(vals, dvals, sizeof(double) * nfull, cudaMemcpyDeviceToHost, s));
+    NFFTK_CUDA(cudaMemcpyAsync(idx, didx, sizeof(int64_t) * nfull, cudaMemcpyDeviceToHost, s));
+    NFFTK_CUDA(cudaMemcpyAsync(counts, dcnt, sizeof(int64_t) * p->M, cudaMemcpyDeviceToHost, s));
+  }
+  NFFTK_CUDA(cudaFreeAsync(dpsi, s));
+  if (vals) {
+    NFFTK_CUDA(cudaFreeAsync(dvals, s));
+    NFFTK_CUDA(cudaFreeAsync(didx, s));
+    NFFTK_CUDA(cudaFreeAsync(dcnt, s));
+  }
+  NFFTK_CUDA(cudaStreamSynchronize(s));
+}
+
+// PrecomputeTables.lut / lut_steps (plan.py:285-295) of a PRE_LIN_PSI plan
+void plan_lut_tables(Plan* p, double* lut, double* steps) {
+  if (!p->ready || !p->lut) fail(EK_STATE, "no PRE_LIN_PSI table; set the flag and call precompute()");
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  NFFTK_CUDA(cudaMemcpy(lut, p->lut, sizeof(double) * p->d * (LUT_SIZE + 1), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < p->d; ++i) steps[i] = p->geom.lut_step[i];
 }
 
 void plan_bind_grid(Plan* p, void* dev, int64_t bytes) {

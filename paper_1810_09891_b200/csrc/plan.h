@@ -124,9 +124,13 @@ void plan_ndft_device(Plan* p, const void* in, void* out, bool adjoint, cudaStre
 void plan_ndft_host(Plan* p, const double* in, double* out, bool adjoint);
 void plan_node_order(Plan* p, int64_t* out);
 void plan_bind_grid(Plan* p, void* dev, int64_t bytes);
+void plan_psi_tables(Plan* p, double* psi, double* vals, int64_t* idx, int64_t* counts);
+void plan_lut_tables(Plan* p, double* lut, double* steps);
 void plan_phase_times(Plan* p, double* ms, int64_t* calls, int nmax, int reset);
 std::vector<double> plan_phi_hut(const Plan* p, int dim);
 double host_window(int code, double t, double n_i, double m, double b_i);
 double host_bessel_i0(double x);
+int phi_hat_value(int code, int k, int n_i, int m, double b, double* out);
+double window_shape(int code, int N_i, int n_i, int m);
 
 }  // namespace nfftk

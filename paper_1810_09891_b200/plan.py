@@ -9,7 +9,6 @@ path: zero-copy, ordered on the current torch stream, returns a tensor).
 
 import ctypes
 import math
-from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -72,33 +71,46 @@ def default_n(N):
     return tuple(1 << ((v - 1).bit_length() + 1) for v in N)
 
 
-@dataclass
 class PrecomputeTables:
-    """Host view of what precompute built (plan.py:109-121).  The window
-    factor table itself (PRE_PSI) lives on the device in tile-sorted order;
-    ``psi_on_device`` reports it instead of a host array."""
+    """What precompute built (reference plan.py:109-121): ``phi_hut``,
+    ``psi`` (M, d, 2m+1), ``psi_full_vals`` / ``psi_full_idx`` (M, (2m+1)^d)
+    and ``psi_full_counts``, ``lut`` (d, 2^14+1) and ``lut_steps``,
+    ``node_order``, ``window_evals``.  Entries the plan's f1 does not request
+    are None, as in the reference.
 
-    phi_hut: list = None
-    psi: np.ndarray = None
-    psi_on_device: bool = False
-    lut_on_device: bool = False
-    window_evals: int = 0
-    # node_order (plan.py:120, :296) is materialised on first access: at C5
-    # it is a 512 MiB int64 host array from a device lexsort, which the
-    # transforms never need
-    _order_source: object = field(default=None, repr=False, compare=False)
-    _node_order: np.ndarray = field(default=None, repr=False, compare=False)
+    The transforms read their tables on the device, in their own layouts;
+    the host arrays above are materialised on first access (device kernels
+    in the reference layout and natural node order, then one copy): at C5
+    ``psi`` alone is 14.5 GB, which a caller that never inspects it should not
+    pay for.  ``psi_on_device`` / ``lut_on_device`` say what the device holds.
+    """
 
-    @property
-    def node_order(self):
-        if self._node_order is None and self._order_source is not None:
-            self._node_order = self._order_source()
-        return self._node_order
+    _LAZY = ("psi", "psi_full_vals", "psi_full_idx", "psi_full_counts", "lut", "lut_steps", "node_order")
 
-    @node_order.setter
-    def node_order(self, value):
-        self._node_order = value
-        self._order_source = None
+    def __init__(self, phi_hut=None, window_evals=0, psi_on_device=False, lut_on_device=False,
+                 sources=None):
+        self.phi_hut = phi_hut
+        self.window_evals = window_evals
+        self.psi_on_device = psi_on_device
+        self.lut_on_device = lut_on_device
+        self._sources = dict(sources or {})
+
+    def __getattr__(self, name):
+        if name in PrecomputeTables._LAZY:
+            src = self.__dict__.get("_sources", {}).pop(name, None)
+            value = src() if src is not None else None
+            if isinstance(value, dict):  # one source filling several fields
+                for k, v in value.items():
+                    self.__dict__[k] = v
+                    self._sources.pop(k, None)
+                return self.__dict__[name]
+            self.__dict__[name] = value
+            return value
+        raise AttributeError(name)
+
+    def __repr__(self):
+        return (f"PrecomputeTables(phi_hut={'set' if self.phi_hut is not None else None}, "
+                f"lazy={sorted(self._sources)}, window_evals={self.window_evals})")
 
 
 def _is_torch(a):
@@ -290,19 +302,48 @@ class Plan:
         p = self._params()
         if not p[8]:
             return None
-        t = PrecomputeTables()
-        if self.f1 & PRE_PHI_HUT:
-            t.phi_hut = [self.phi_hut(i) for i in range(self.d)]
-        t.psi_on_device = p[9] == MODE_TENSOR
-        t.lut_on_device = bool(self.f1 & PRE_LIN_PSI)
         evals = 0
         if self.f1 & (PRE_PSI | PRE_FULL_PSI):
             evals += int(p[12])
         if self.f1 & PRE_LIN_PSI:
             evals += self.d * (LUT_SIZE + 1)
-        t.window_evals = evals
-        t._order_source = lambda: self.node_order
-        return t
+        sources = {"node_order": lambda: self.node_order}
+        if self.f1 & (PRE_PSI | PRE_FULL_PSI):
+            full = bool(self.f1 & PRE_FULL_PSI)
+            fill = lambda: self._psi_tables(full)  # noqa: E731
+            for k in (("psi",) if self.f1 & PRE_PSI else ()) + \
+                    (("psi_full_vals", "psi_full_idx", "psi_full_counts") if full else ()):
+                sources[k] = fill
+        if self.f1 & PRE_LIN_PSI:
+            sources["lut"] = sources["lut_steps"] = self._lut_tables
+        return PrecomputeTables(
+            phi_hut=[self.phi_hut(i) for i in range(self.d)] if self.f1 & PRE_PHI_HUT else None,
+            window_evals=evals, psi_on_device=p[9] == MODE_TENSOR,
+            lut_on_device=bool(self.f1 & PRE_LIN_PSI), sources=sources)
+
+    def _psi_tables(self, full):
+        """Reference-layout psi (and PRE_FULL_PSI tables) from the device."""
+        K = 2 * self.m + 1
+        psi = np.empty((self.M, self.d, K))
+        out = {"psi": psi if self.f1 & PRE_PSI else None}
+        vals = idx = counts = None
+        if full:
+            P = K ** self.d
+            vals = np.empty((self.M, P))
+            idx = np.empty((self.M, P), dtype=np.int64)
+            counts = np.empty(self.M, dtype=np.int64)
+            out.update(psi_full_vals=vals, psi_full_idx=idx, psi_full_counts=counts)
+        ptr = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else None  # noqa: E731
+        self._check(self._lib_checked().nfftk_psi_tables(self._h, ptr(psi), ptr(vals), ptr(idx),
+                                                         ptr(counts), psi.size))
+        return out
+
+    def _lut_tables(self):
+        lut = np.empty((self.d, LUT_SIZE + 1))
+        steps = np.empty(self.d)
+        self._check(self._lib_checked().nfftk_lut_tables(self._h, ctypes.c_void_p(lut.ctypes.data),
+                                                         ctypes.c_void_p(steps.ctypes.data), lut.size))
+        return {"lut": lut, "lut_steps": steps}
 
     def phi_hut(self, i):
         out = np.empty(self.N[i] + 1)

@@ -1,64 +1,49 @@
-"""Window model of a plan (kind, sigma, b) with host evaluators.
+"""Window model of a plan: kind, oversampling factors and shape parameters.
 
-Same closed forms as the reference (window.py:56-181): Kaiser-Bessel
-phi(t) = sinh(b sqrt(m^2 - (n t)^2)) / (pi sqrt(.)) with b = pi (2 - 1/sigma),
-phi_hat(k) = I0(m sqrt(b^2 - (2 pi k / n)^2)) / n; Gaussian
-phi(t) = exp(-(n t)^2 / b) / sqrt(pi b), b = 2 sigma m / ((2 sigma - 1) pi),
-phi_hat(k) = exp(-b (pi k / n)^2) / n.  These host evaluators serve the
-Python API (``plan.window.phi`` ...); the transforms evaluate the window on
-the device (csrc/common.cuh) and build phi_hat in the C library.
-The quadrature oracle ``phi_hat_oracle`` of the reference is test-only and
-not part of this package.
+The closed forms (Kaiser-Bessel and Gaussian phi, phi_hat, the I0 series;
+reference window.py:38-181) are implemented ONCE, in the C library
+(csrc/plan.cu host math, csrc/common.cuh device math).  This class keeps the
+reference's ``WindowModel`` interface -- ``make`` with its validation, ``b``,
+``phi``, ``psi``, ``phi_hat``, ``phi_hat_table``, ``ck`` -- and evaluates
+through ``nfftk_window_b`` / ``nfftk_window_values`` / ``nfftk_phi_hat_values``
+in batches.  The reference's quadrature oracle ``phi_hat_oracle`` is test
+infrastructure and is not part of this package.
 """
 
-import math
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _lib
 from .errors import NfftError, ShapeError, WindowDegenerateError
 
 KAISER_BESSEL = 0
 GAUSSIAN = 1
-_KIND_BY_NAME = {"kaiserbessel": KAISER_BESSEL, "gaussian": GAUSSIAN}
-
-
-def bessel_i0(x):
-    """I0 power series, term-ratio cutoff 1e-16 (window.py:38-53)."""
-    s = t = 1.0
-    q = 0.25 * x * x
-    j = 0
-    while True:
-        j += 1
-        t *= q / (j * j)
-        s += t
-        if t < 1e-16 * s:
-            return s
-
-
-def window_factor(code, t, n_i, m, b_i):
-    """Scalar window value at offset t (window.py:56-72)."""
-    if code == KAISER_BESSEL:
-        u = m * m - (n_i * t) * (n_i * t)
-        if u > 0.0:
-            z = math.sqrt(u)
-            return math.sinh(b_i * z) / (math.pi * z)
-        if u < 0.0:
-            z = math.sqrt(-u)
-            return math.sin(b_i * z) / (math.pi * z)
-        return b_i / math.pi
-    return math.exp(-(n_i * t) * (n_i * t) / b_i) / math.sqrt(math.pi * b_i)
+WINDOW_CODES = {"kaiserbessel": KAISER_BESSEL, "gaussian": GAUSSIAN}
 
 
 def kind_code(kind):
-    code = _KIND_BY_NAME.get(str(kind).lower())
-    if code is None:
-        raise NfftError(f"unknown window {kind!r}; use 'kaiserbessel' or 'gaussian'")
-    return code
+    """Library code of a window name (case-insensitive)."""
+    try:
+        return WINDOW_CODES[str(kind).lower()]
+    except KeyError:
+        raise NfftError(f"unknown window {kind!r}; use 'kaiserbessel' or 'gaussian'") from None
+
+
+def bessel_i0(x):
+    """The library's I0 power series (window.py:38-53)."""
+    return float(_lib.load().nfftk_bessel_i0(float(x)))
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
 
 
 @dataclass(frozen=True)
 class WindowModel:
+    """Per-dimension window parameters: sigma_i = n_i / N_i, shape b_i."""
+
     kind: str
     code: int
     n: tuple
@@ -68,23 +53,20 @@ class WindowModel:
 
     @classmethod
     def make(cls, kind, N, n, m):
+        """Validated model (window.py:91-112 rules and messages)."""
         code = kind_code(kind)
-        N = tuple(int(v) for v in N)
-        n = tuple(int(v) for v in n)
-        m = int(m)
+        N, n, m = tuple(map(int, N)), tuple(map(int, n)), int(m)
         if len(N) != len(n):
             raise ShapeError("bandlimit and grid vectors differ in length")
         sigma = tuple(ni / Ni for ni, Ni in zip(n, N))
-        for s in sigma:
-            if s <= 1.0:
-                raise NfftError(f"oversampling factor must exceed 1, got sigma={s}")
-        for ni in n:
-            if m / ni >= 0.5:
-                raise NfftError(f"window support m/n={m}/{ni} must be below 1/2")
-        if code == KAISER_BESSEL:
-            b = tuple(math.pi * (2.0 - 1.0 / s) for s in sigma)
-        else:
-            b = tuple(2.0 * s * m / ((2.0 * s - 1.0) * math.pi) for s in sigma)
+        bad = [s for s in sigma if not s > 1.0]
+        if bad:
+            raise NfftError(f"oversampling factor must exceed 1, got sigma={bad[0]}")
+        wide = [ni for ni in n if not m / ni < 0.5]
+        if wide:
+            raise NfftError(f"window support m/n={m}/{wide[0]} must be below 1/2")
+        lib = _lib.load()
+        b = tuple(float(lib.nfftk_window_b(code, Ni, ni, m)) for Ni, ni in zip(N, n))
         return cls(kind=str(kind).lower(), code=code, n=n, sigma=sigma, m=m, b=b)
 
     @property
@@ -92,51 +74,57 @@ class WindowModel:
         return len(self.n)
 
     def _dim(self, i):
-        if not 0 <= i < self.d:
+        if i < 0 or i >= self.d:
             raise ShapeError(f"dimension index {i} outside [0, {self.d})")
         return i
 
     def phi(self, t, i=0):
+        """phi_i at offsets t (scalar in, scalar out)."""
         i = self._dim(i)
-        t = np.asarray(t, dtype=np.float64)
-        f = np.vectorize(lambda v: window_factor(self.code, float(v), float(self.n[i]),
-                                                 float(self.m), self.b[i]), otypes=[float])
-        out = f(t)
-        return float(out) if t.ndim == 0 else out
+        arr = np.ascontiguousarray(t, dtype=np.float64)
+        flat = arr.reshape(-1)
+        out = np.empty_like(flat)
+        _lib.load().nfftk_window_values(self.code, float(self.n[i]), self.m, self.b[i], _ptr(flat),
+                                        flat.size, _ptr(out))
+        return float(out[0]) if arr.ndim == 0 else out.reshape(arr.shape)
 
     def psi(self, t, i=0):
-        i = self._dim(i)
+        """phi_i truncated to its support |t| <= m / n_i."""
         t = np.asarray(t, dtype=np.float64)
-        return np.where(np.abs(t) <= self.m / self.n[i], self.phi(t, i), 0.0)
+        inside = np.abs(t) <= self.m / self.n[self._dim(i)]
+        return np.where(inside, self.phi(t, i), 0.0)
+
+    def _phi_hat_many(self, ks, i):
+        ks = np.ascontiguousarray(ks, dtype=np.int32)
+        over = np.abs(ks) > self.n[i] // 2
+        if over.any():
+            k = int(ks[over][0])
+            raise NfftError(f"|k|={abs(k)} exceeds n/2={self.n[i] // 2}")
+        vals = np.empty(ks.size)
+        status = np.empty(ks.size, dtype=np.int32)
+        _lib.load().nfftk_phi_hat_values(self.code, self.n[i], self.m, self.b[i], _ptr(ks), ks.size,
+                                         _ptr(vals), _ptr(status))
+        if status.any():
+            j = int(np.flatnonzero(status)[0])
+            k = int(ks[j])
+            if status[j] == 1:
+                raise WindowDegenerateError(f"{self.kind} transform vanishes at k={k}")
+            raise WindowDegenerateError(f"window transform not positive at k={k}: {vals[j]}")
+        return vals
 
     def phi_hat(self, k, i=0):
-        i = self._dim(i)
-        k = int(k)
-        n_i = self.n[i]
-        if abs(k) > n_i // 2:
-            raise NfftError(f"|k|={abs(k)} exceeds n/2={n_i // 2}")
-        if self.code == KAISER_BESSEL:
-            arg = self.b[i] ** 2 - (2.0 * math.pi * k / n_i) ** 2
-            if arg < 0.0:
-                raise WindowDegenerateError(f"kaiserbessel transform vanishes at k={k}")
-            val = bessel_i0(self.m * math.sqrt(arg)) / n_i
-        else:
-            val = math.exp(-self.b[i] * (math.pi * k / n_i) ** 2) / n_i
-        if not val > 0.0:
-            raise WindowDegenerateError(f"window transform not positive at k={k}: {val}")
-        return val
+        """phi_hat_i(k), strictly positive (window.py:142-164)."""
+        return float(self._phi_hat_many([int(k)], self._dim(i))[0])
 
     def phi_hat_table(self, i=0, kmax=None):
+        """phi_hat_i over k = -kmax .. kmax (default n_i / 2)."""
         i = self._dim(i)
-        if kmax is None:
-            kmax = self.n[i] // 2
-        return np.array([self.phi_hat(k, i) for k in range(-kmax, kmax + 1)])
+        kmax = self.n[i] // 2 if kmax is None else int(kmax)
+        return self._phi_hat_many(np.arange(-kmax, kmax + 1), i)
 
     def ck(self, k):
+        """Tensor-product coefficient prod_i phi_hat_i(k_i)."""
         k = np.atleast_1d(np.asarray(k, dtype=np.int64))
         if k.shape[0] != self.d:
             raise ShapeError(f"multi-index has {k.shape[0]} dims, window has {self.d}")
-        out = 1.0
-        for i in range(self.d):
-            out *= self.phi_hat(int(k[i]), i)
-        return out
+        return float(np.prod([self.phi_hat(int(k[i]), i) for i in range(self.d)]))

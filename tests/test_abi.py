@@ -15,7 +15,7 @@ from paper_1810_09891_b200 import _lib, abi
 REF = json.load(open(os.path.join(GOLDEN, "abi_reference.json")))
 
 CTYPE = {"int32_t": ctypes.c_int32, "int64_t": ctypes.c_int64, "uint32_t": ctypes.c_uint32,
-         "uint64_t": ctypes.c_uint64}
+         "uint64_t": ctypes.c_uint64, "double": ctypes.c_double}
 
 
 def test_reference_symbols_identical():

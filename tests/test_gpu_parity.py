@@ -474,3 +474,59 @@ def test_distributed_plan_single_rank_matches_plan(torch):
     assert e2(c["trafo"], f) < TOL128
     assert e2(c["adjoint"], a) < TOL128
     dp.close()
+
+
+# ------------------------------------------------ PrecomputeTables contents
+@pytest.mark.parametrize("name", ["d1_small", "d2_aligned", "d3_aligned", "d3_m6"])
+def test_tables_psi_in_reference_layout(name, oracle):
+    """tables.psi (M, d, 2m+1) and the PRE_FULL_PSI tables (plan.py:109-121,
+    kernels.py:56-119) materialised from the device in natural node order:
+    the window at x - (lo + t)/n, zero past the width; products in
+    lexicographic order with their flat wrapped cells."""
+    c = dict(case(name))
+    c["f1"] = np.array(nf.PRE_PHI_HUT | nf.PRE_PSI | nf.PRE_FULL_PSI)
+    p = make_plan(c)
+    t = p.tables
+    x, n, m = c["x"], tuple(int(v) for v in c["n"]), int(c["m"])
+    M, d = x.shape
+    K = 2 * m + 1
+    lo, width = oracle.node_ranges(n, m, x)
+    b = [oracle.window_b(0, int(Ni), int(ni), m) for Ni, ni in zip(c["N"], n)]
+    ref = np.zeros((M, d, K))
+    for j in range(M):
+        for i in range(d):
+            for k in range(width[j, i]):
+                ref[j, i, k] = oracle.window_factor(0, x[j, i] - (lo[j, i] + k) / n[i], n[i], m, b[i])
+    assert t.psi.shape == (M, d, K)
+    assert np.allclose(t.psi, ref, rtol=1e-14, atol=0)
+    vals, idx, counts = t.psi_full_vals, t.psi_full_idx, t.psi_full_counts
+    assert vals.shape == (M, K ** d) and idx.shape == (M, K ** d)
+    assert np.array_equal(counts, np.prod(width, axis=1))
+    for j in range(M):
+        cells = [np.mod(lo[j, i] + np.arange(width[j, i]), n[i]) for i in range(d)]
+        facs = [t.psi[j, i, :width[j, i]] for i in range(d)]
+        prod, flat = facs[0], cells[0]
+        for i in range(1, d):
+            prod = (prod[:, None] * facs[i][None, :]).ravel()
+            flat = (flat[:, None] * n[i] + cells[i][None, :]).ravel()
+        assert np.array_equal(vals[j, :counts[j]], prod)
+        assert np.array_equal(idx[j, :counts[j]], flat)
+        assert not vals[j, counts[j]:].any() and not idx[j, counts[j]:].any()
+
+
+def test_tables_lut_and_absent_entries(oracle):
+    from paper_1810_09891_b200.plan import LUT_SIZE
+
+    c = dict(case("d2_lut"))
+    p = make_plan(c)
+    t = p.tables
+    assert t.psi is None and t.psi_full_vals is None
+    n, m = tuple(int(v) for v in c["n"]), int(c["m"])
+    assert t.lut.shape == (2, LUT_SIZE + 1)
+    for i in range(2):
+        b = oracle.window_b(0, int(c["N"][i]), n[i], m)
+        h = (m / n[i]) / LUT_SIZE
+        for s in (0, 1, 777, LUT_SIZE):
+            ref = oracle.window_factor(0, s * h, n[i], m, b)
+            assert abs(t.lut[i, s] - ref) <= 1e-15 * abs(ref)
+        assert t.lut_steps[i] == LUT_SIZE / (m / n[i])
