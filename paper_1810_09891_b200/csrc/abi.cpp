@@ -429,14 +429,18 @@ int32_t nfftk_bind_grid(int32_t h, void* dev, int64_t bytes) {
   return guarded(e, [&] { plan_bind_grid(e->plan, dev, bytes); });
 }
 
-// params: [d, M, m, window, precision, f1, f2, has_nodes, ready, mode, ntiles, nsubs, width_sum]
+// params: [d, M, m, window, precision, f1, f2, has_nodes, ready, mode, ntiles, nsubs, width_sum,
+//          gridding kernels (0 batch, 1 pipelined row-per-thread, 2 residue-owned), wide nodes]
 int32_t nfftk_get_params(int32_t h, int64_t* out, int32_t count) {
   EntryLock e(h);
   if (!e) return ERR_HANDLE;
   Plan* p = e->plan;
-  int64_t v[13] = {p->d, p->M, p->m, p->window, p->single ? 1 : 0, (int64_t)p->f1, (int64_t)p->f2,
-                   p->has_nodes, p->ready, p->mode, p->ntiles, p->nsubs, (int64_t)p->width_sum};
-  for (int i = 0; i < count && i < 13; ++i) out[i] = v[i];
+  const bool tensor = p->ready && p->mode == MODE_TENSOR && p->d <= MAX_D;
+  const int path = !tensor ? 0 : (res_ok(p->geom) ? 2 : (pipe_geometry(p->geom) ? 1 : 0));
+  int64_t v[15] = {p->d, p->M, p->m, p->window, p->single ? 1 : 0, (int64_t)p->f1, (int64_t)p->f2,
+                   p->has_nodes, p->ready, p->mode, p->ntiles, p->nsubs, (int64_t)p->width_sum,
+                   path, p->geom.nwide};
+  for (int i = 0; i < count && i < 15; ++i) out[i] = v[i];
   return 0;
 }
 

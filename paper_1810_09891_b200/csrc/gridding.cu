@@ -27,138 +27,12 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
 namespace nfftk {
 
-__device__ __forceinline__ size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
-
-template <int D>
-__device__ __forceinline__ void tile_of(const Geom& g, int tile, int* tc) {
-  int t = tile;
-#pragma unroll
-  for (int i = D - 1; i >= 0; --i) {
-    tc[i] = t % g.ntile[i];
-    t /= g.ntile[i];
-  }
-}
-
-// ------------------------------------------------------- async copy PTX
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sdst)), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sdst)), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-template <typename C>
-__device__ __forceinline__ void cp_async_cell(C* sdst, const C* gsrc) {
-  if constexpr (sizeof(C) == 16) cp_async16(sdst, gsrc);
-  else cp_async8(sdst, gsrc);
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes));
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// TMA: L2 prefetch of a halo box (no shared-memory destination)
-__device__ __forceinline__ void tma_prefetch_box3(const CUtensorMap* tm, const int* c) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(tm),
-               "r"(c[0]), "r"(c[1]), "r"(c[2])
-               : "memory");
-}
-
-// TMA: whole halo box of the padded grid -> shared memory
-template <int D>
-__device__ __forceinline__ void tma_load_box(void* sdst, const CUtensorMap* tm, const int* c,
-                                             unsigned long long* bar) {
-  if constexpr (D == 3) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(sdst)),
-        "l"(tm), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(smem_u32(bar))
-        : "memory");
-  } else if constexpr (D == 2) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(sdst)),
-        "l"(tm), "r"(c[0]), "r"(c[1]), "r"(smem_u32(bar))
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(sdst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// TMA bulk reduction shared -> global (L2 performs the adds)
-template <typename R>
-__device__ __forceinline__ void bulk_red_add(void* gdst, const void* ssrc, unsigned bytes) {
-  if constexpr (sizeof(R) == 8)
-    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst),
-                 "r"(smem_u32(ssrc)), "r"(bytes)
-                 : "memory");
-  else
-    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
-                 "r"(smem_u32(ssrc)), "r"(bytes)
-                 : "memory");
-}
-// One staged halo row into the DENSE grid: cells [c0, c0 + len) of the row
-// starting at dense index rowbase, c0 in [-n2, n2), wrapped periodically
-// (kernels.py:47 slot arithmetic) -- at most two bulk reductions.  Both
-// pieces stay 16-byte aligned: c128 cells are 16 bytes; c64 needs c0, len
-// and n2 even (spread_dense_ok).
-template <typename R>
-__device__ __forceinline__ void bulk_red_row_wrapped(cplx_t<R>* grid, int64_t rowbase, int c0, int n2,
-                                                     const cplx_t<R>* src, int len) {
-  const int c = c0 < 0 ? c0 + n2 : c0;
-  const int first = min(len, n2 - c);
-  bulk_red_add<R>(grid + rowbase + c, src, (unsigned)(first * sizeof(cplx_t<R>)));
-  if (first < len)
-    bulk_red_add<R>(grid + rowbase, src + first, (unsigned)((len - first) * sizeof(cplx_t<R>)));
-}
-
-__device__ __forceinline__ void bulk_commit_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;\n" ::);
-  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
 
 // ----------------------------------------------------------- node batches
 // coordinates [D][NB], window factors [NB][D*K] (PRE_PSI rows copied, or
@@ -2276,6 +2150,10 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
 void launch_interp(bool single, const void* tmap, const void* gp, void* f, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
+  if (!single && res_ok(g)) {  // tmap: the plan's 15^3-box map
+    launch_interp_res(tmap, gp, f, xs, perm, subs, nsubs, g, s);
+    return;
+  }
   const CUtensorMap* tm = (const CUtensorMap*)tmap;
   if (single) NFFTK_DISPATCH_DM(interp_go, float, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);
   else NFFTK_DISPATCH_DM(interp_go, double, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);
@@ -2284,6 +2162,10 @@ void launch_interp(bool single, const void* tmap, const void* gp, void* f, const
 void launch_spread(bool single, void* gp, const void* f, void* fs, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
+  if (!single && res_ok(g)) {  // gp: the dense grid (dense_flush)
+    launch_spread_res(gp, fs, xs, subs, nsubs, g, s);
+    return;
+  }
   const CUtensorMap* tm = nullptr;
   if (single) NFFTK_DISPATCH_DM(spread_go, float, tm, gp, f, fs, xs, perm, subs, nsubs, g, s);
   else NFFTK_DISPATCH_DM(spread_go, double, tm, gp, f, fs, xs, perm, subs, nsubs, g, s);

@@ -74,7 +74,14 @@ __global__ void k_bin_keys(const double* __restrict__ x, int64_t M, Geom g,
       tile = tile * g.ntile[dim] + tcoord;
       lc[dim] = (uint32_t)(s - (int64_t)tcoord * g.T[dim]);
     }
-    for (int dim = g.d - 1; dim >= 0; --dim) local = local * g.T[dim] + lc[dim];
+    if (g.res) {
+      // residue kernels: runs of equal dim-1 cell, dim 0 in serpentine order
+      // inside them (a lane's row changes when the dim-0 / dim-1 cell passes
+      // its residue: residue.cu), last dim least significant
+      local = (lc[1] * 8 + ((lc[1] & 1) ? 7 - lc[0] : lc[0])) * 8 + lc[2];
+    } else {
+      for (int dim = g.d - 1; dim >= 0; --dim) local = local * g.T[dim] + lc[dim];
+    }
     uint32_t tvol = 1;
     for (int dim = 0; dim < g.d; ++dim) tvol *= g.T[dim];
     keys[i] = tile * tvol + local;
@@ -143,6 +150,11 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
       t = r - blk * (K + 1);
       dim = blk == 0 ? g.d - 1 : (blk == 1 ? 0 : (blk == 2 ? 1 : g.d));
       if (t >= K) dim = g.d;  // the block's zero / row padding
+    } else if (g.psi_pad == 3) {
+      // residue rows: blocks of 2m -- last dim, dim 0, dim 1 (common.cuh RES_PR)
+      const int blk = r / (K - 1);
+      t = r - blk * (K - 1);
+      dim = blk == 0 ? g.d - 1 : (blk == 1 ? 0 : (blk == 2 ? 1 : g.d));
     } else {
       dim = r / K;
       t = r - dim * K;
@@ -208,10 +220,14 @@ __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict
     } else if (g.psi_pad == 2) {
       // sten3 blocks: last dim, dim 0, dim 1 (common.cuh)
       pos = dim == g.d - 1 ? STEN3_OW2 : (dim == 0 ? sten3_ow0(K) : sten3_ow1(K));
+    } else if (g.psi_pad == 3) {
+      // residue rows: blocks of 2m factors (a wide node's last factor is dropped;
+      // k_wide_nodes evaluates those nodes directly)
+      pos = dim == g.d - 1 ? 0 : (dim == 0 ? K - 1 : 2 * (K - 1));
     }
     slo[nd] = st.lo;
     spos[nd] = pos;
-    swid[nd] = st.width;
+    swid[nd] = g.psi_pad == 3 ? min(st.width, K - 1) : st.width;
   }
   __syncthreads();
   const int items = nn * g.d * K;
@@ -251,7 +267,8 @@ void build_psi(const double* xs, int64_t M, const Geom& g, void* psi, cudaStream
 // k_bin_keys assigned (same slot arithmetic), so the spread reads one 16-byte
 // record per node instead of recomputing stencils from coordinates.
 __global__ void k_build_recs(const double* __restrict__ xs, int64_t M, Geom g,
-                             int4* __restrict__ rec) {
+                             int4* __restrict__ rec, unsigned* __restrict__ rrec,
+                             unsigned* __restrict__ nwide) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
        i += (int64_t)gridDim.x * blockDim.x) {
     int h[3] = {0, 0, 0};
@@ -267,11 +284,18 @@ __global__ void k_build_recs(const double* __restrict__ xs, int64_t M, Geom g,
     }
     packed |= (unsigned)fast << 24;
     rec[i] = make_int4(h[0], h[1], h[2], (int)packed);
+    if (rrec) {
+      // residue record (common.cuh RES_*): a regular node's halo start is its
+      // cell inside the tile (h - 1 in the 15^3 halo)
+      rrec[i] = fast ? ((unsigned)(h[0] - 1) | (unsigned)(h[1] - 1) << 3 | (unsigned)(h[2] - 1) << 6 | RES_REGULAR) : 0u;
+      if (!fast) atomicAdd(nwide, 1u);
+    }
   }
 }
 
-void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, cudaStream_t s) {
-  k_build_recs<<<blocks_for(M, 256), 256, 0, s>>>(xs, M, g, rec);
+void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, unsigned* rrec, unsigned* nwide,
+                cudaStream_t s) {
+  k_build_recs<<<blocks_for(M, 256), 256, 0, s>>>(xs, M, g, rec, rrec, nwide);
   count_launch();
 }
 
@@ -382,6 +406,28 @@ __global__ void k_sub_keys(const int4* __restrict__ subs, int total, int maxsub,
   vals[i] = i;
 }
 
+// d = 3: subproblems in blocks of 4 x 4 x ntile[2] tiles
+// (dim-0 / dim-1 neighbours stay within ~256 subproblems, so the halo overlap
+// of neighbouring tiles -- the spread's reductions, the interp's box loads --
+// meets in L2 instead of HBM), in three weight classes around the mean count
+// so that evenly filled tiles keep one order.
+__global__ void k_sub_keys_res(const int4* __restrict__ subs, int total, int mean, Geom g,
+                               uint32_t* __restrict__ keys, int* __restrict__ vals) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int4 sp = subs[i];
+  int t = sp.x;
+  const int k = t % g.ntile[2];
+  t /= g.ntile[2];
+  const int j = t % g.ntile[1], a = t / g.ntile[1];
+  const uint32_t nb1 = (uint32_t)(g.ntile[1] + 3) / 4;
+  const uint32_t blk = ((uint32_t)(a / 4) * nb1 + (uint32_t)(j / 4)) * 16u + (uint32_t)((a % 4) * 4 + (j % 4));
+  const uint32_t cls = sp.z > 2 * mean ? 0u : (2 * sp.z >= mean ? 1u : 2u);
+  const uint32_t nblk = (uint32_t)((g.ntile[0] + 3) / 4) * nb1 * 16u;
+  keys[i] = (cls * nblk + blk) * (uint32_t)g.ntile[2] + (uint32_t)k;
+  vals[i] = i;
+}
+
 __global__ void k_gather_subs(const int4* __restrict__ subs, const int* __restrict__ order, int total,
                               int4* __restrict__ out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,13 +509,20 @@ void bin_and_sort(const double* x_dev, int64_t M, const Geom& g, int maxsub, int
     NFFTK_CUDA(cudaMallocAsync(&sk, sizeof(uint32_t) * total * 2, s));
     NFFTK_CUDA(cudaMallocAsync(&sv, sizeof(int) * total * 2, s));
     NFFTK_CUDA(cudaMalloc(&sorted, sizeof(int4) * total));
-    k_sub_keys<<<(total + 255) / 256, 256, 0, s>>>(*subs, total, maxsub, sk, sv);
+    int key_bits = 3;
+    if (g.d == 3 && !getenv("NFFTK_NO_BLOCK_ORDER")) {
+      const int mean = (int)std::max<int64_t>(1, M / std::max(1, ntiles));
+      k_sub_keys_res<<<(total + 255) / 256, 256, 0, s>>>(*subs, total, mean, g, sk, sv);
+      key_bits = bits_for(3ull * ((g.ntile[0] + 3) / 4) * ((g.ntile[1] + 3) / 4) * 16ull * g.ntile[2]);
+    } else {
+      k_sub_keys<<<(total + 255) / 256, 256, 0, s>>>(*subs, total, maxsub, sk, sv);
+    }
     count_launch();
     size_t lb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, lb, sk, sk + total, sv, sv + total, total, 0, 3, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, lb, sk, sk + total, sv, sv + total, total, 0, key_bits, s);
     void* ltmp = nullptr;
     NFFTK_CUDA(cudaMallocAsync(&ltmp, lb, s));
-    NFFTK_CUDA(cub::DeviceRadixSort::SortPairs(ltmp, lb, sk, sk + total, sv, sv + total, total, 0, 3, s));
+    NFFTK_CUDA(cub::DeviceRadixSort::SortPairs(ltmp, lb, sk, sk + total, sv, sv + total, total, 0, key_bits, s));
     count_launch();
     k_gather_subs<<<(total + 255) / 256, 256, 0, s>>>(*subs, sv + total, total, sorted);
     count_launch();

@@ -132,6 +132,7 @@ Plan::~Plan() {
   cudaFree(subs);
   cudaFree(psi);
   cudaFree(rec);
+  cudaFree(rrec);
   cudaFree(lut);
   cudaFree(cols);
   if (!grid_external) cudaFree(grid);
@@ -236,6 +237,7 @@ static void choose_tiles(Plan* p) {
   while (ms > 32 && (int64_t)ms * 4 * 148 > p->M) ms /= 2;
   p->maxsub = env_int("NFFTK_MAXSUB", ms);
   g.debug = env_int("NFFTK_DEBUG", 0);
+  g.res = res_geometry(g, p->single) ? 1 : 0;
 }
 
 static void fill_geom(Plan* p) {
@@ -423,8 +425,23 @@ static void nodes_to_device(Plan* p, cudaStream_t s) {
                p->tile_start, &p->subs, &p->nsubs, s);
   p->width_sum = sum_widths(p->xs, M, p->geom, s);
   if (!p->rec) NFFTK_CUDA(cudaMalloc(&p->rec, sizeof(int4) * M));
-  build_recs(p->xs, M, p->geom, p->rec, s);
+  unsigned* nwide = nullptr;
+  if (p->geom.res) {
+    // +4: aligned bulk copies; the wide-node counter sits behind them
+    if (!p->rrec) NFFTK_CUDA(cudaMalloc(&p->rrec, sizeof(unsigned) * (M + 8)));
+    nwide = p->rrec + M + 4;
+    NFFTK_CUDA(cudaMemsetAsync(p->rrec + M, 0, sizeof(unsigned) * 8, s));
+  }
+  build_recs(p->xs, M, p->geom, p->rec, p->geom.res ? p->rrec : nullptr, nwide, s);
   p->geom.rec = p->rec;
+  p->geom.rrec = p->rrec;
+  p->geom.nwide = 0;
+  if (nwide) {
+    unsigned cnt = 0;
+    NFFTK_CUDA(cudaMemcpyAsync(&cnt, nwide, sizeof cnt, cudaMemcpyDeviceToHost, s));
+    NFFTK_CUDA(cudaStreamSynchronize(s));
+    p->geom.nwide = (int)std::min<unsigned>(cnt, 0x7fffffffu);
+  }
 }
 
 // New nodes invalidate the tables; the PRE_PSI allocation itself is kept
@@ -519,6 +536,15 @@ static void build_tensor_map(Plan* p) {
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS) fail(EK_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
+  if (g.res) {
+    // residue interp: the 15^3 halo of regular nodes (residue.cu)
+    for (int i = 0; i < 3; ++i) box[i] = (cuuint32_t)RES_H;
+    box[0] *= scale;
+    res = encode((CUtensorMap*)p->tmap_res, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p->gp, dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) fail(EK_CUDA, "cuTensorMapEncodeTiled (residue box) failed (" + std::to_string((int)res) + ")");
+  }
   p->tmap_ready = true;
 }
 
@@ -610,7 +636,9 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   if (mode == MODE_TENSOR) {
     const int K = 2 * p->m + 1;
     p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? (pipe_sten3(p->single, p->m) ? 2 : 1) : 0;
-    const int pad_count = p->geom.psi_pad == 2 ? sten3_count(K) : psi_row_halo(p->d, p->geom.H, K);
+    if (p->geom.res) p->geom.psi_pad = 3;
+    const int pad_count = p->geom.psi_pad == 3 ? RES_PR
+                          : p->geom.psi_pad == 2 ? sten3_count(K) : psi_row_halo(p->d, p->geom.H, K);
     p->geom.pr = p->geom.psi_pad ? psi_row_pad<double>(pad_count) : psi_row(p->d, K);
     // c64 plans on the pipelined geometries (only the pipelined kernels read
     // the table there) keep fp32 factor rows: half the bytes, no per-FMA
@@ -671,7 +699,8 @@ void plan_interp_device(Plan* p, void* f, cudaStream_t s) {
   NFFTK_CUDA(cudaSetDevice(p->device));
   { PhaseScope ps(p, PH_PAD, s); launch_pad(p->single, p->grid, p->gp, p->pq, s); }
   { PhaseScope ps(p, PH_INTERP, s);
-    launch_interp(p->single, p->tmap, p->gp, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+    launch_interp(p->single, res_ok(p->geom) ? p->tmap_res : p->tmap, p->gp, f, p->xs, p->perm, p->subs,
+                  p->nsubs, p->geom, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }

@@ -55,6 +55,7 @@ struct Plan {
   double* psi = nullptr;
   size_t psi_count = 0;
   int4* rec = nullptr;
+  unsigned* rrec = nullptr;          // residue-kernel node records (+ one counter of wide nodes at [M + 4])
   void* cublas = nullptr;            // cublasHandle_t for the exact sums (lazy)              // per-node stencil records, sorted order
   double* lut = nullptr;
   double* cols = nullptr;
@@ -65,6 +66,7 @@ struct Plan {
   size_t gp_bytes = 0;
   PadGeom pq{};
   alignas(64) unsigned char tmap[128];  // CUtensorMap of gp (halo boxes)
+  alignas(64) unsigned char tmap_res[128];  // CUtensorMap of gp with 15^3 boxes (residue interp)
   bool tmap_ready = false;
   void* fhat_dev = nullptr;
   void* f_dev = nullptr;

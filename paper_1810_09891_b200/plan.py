@@ -186,8 +186,8 @@ class Plan:
 
     # -- plumbing -------------------------------------------------------
     def _params(self):
-        out = (ctypes.c_int64 * 13)()
-        self._lib_checked().nfftk_get_params(self._h, out, 13)
+        out = (ctypes.c_int64 * 15)()
+        self._lib_checked().nfftk_get_params(self._h, out, 15)
         return list(out)
 
     def _lib_checked(self):
@@ -354,6 +354,18 @@ class Plan:
     @property
     def mode(self):
         return int(self._params()[9])
+
+    @property
+    def gridding(self):
+        """Extension: which B / B^H kernels a PRE_PSI plan runs -- "residue"
+        (residue.cu: d=3, m=4, 8^3 tiles), "pipe" (row-per-thread pipelined
+        kernels) or "batch"."""
+        return ("batch", "pipe", "residue")[int(self._params()[13])]
+
+    @property
+    def wide_nodes(self):
+        """Extension: nodes with a 2m+1 wide stencil in some dim (residue geometry only)."""
+        return int(self._params()[14])
 
     @property
     def window_evals_last(self):

@@ -47,6 +47,17 @@ CONFIGS = {
     "C5": Workload("C5", (256, 256, 256), (512, 512, 512), 1 << 26, 4),
 }
 
+# Development sizes (tools/ only): C5's density and cutoff on a grid 8x smaller,
+# for quick kernel A/B runs and ncu captures.
+DEV_CONFIGS = {
+    "C5q": Workload("C5q", (128, 128, 128), (256, 256, 256), 1 << 23, 4),
+}
+
+
+def lookup(name):
+    return CONFIGS.get(name) or DEV_CONFIGS[name]
+
+
 NODE_SEED = 0
 FHAT_SEED = 1
 F_SEED = 2

@@ -1,0 +1,124 @@
+"""Parity of the residue-owned d=3 kernels (residue.cu: k_spread_res,
+k_interp_res, k_wide_nodes) against the CPU oracle: m = 4 on 8^3 tiles,
+complex128.  Cases: grids whose tiles divide n and do not (partial last
+tiles), nodes on every periodic boundary, grid-aligned nodes (2m+1 wide
+stencils: the k_wide_nodes pass), one dense cell (several subproblems of one
+tile), clustered nodes, node counts around the ring's batch sizes, both team
+layouts, and replays of one plan (ticket counters, halo state)."""
+
+import numpy as np
+import pytest
+
+import paper_1810_09891_b200 as nf
+
+pytestmark = pytest.mark.gpu
+
+M4 = 4
+
+
+def e2(ref, got):
+    ref = np.asarray(ref).astype(np.complex128).ravel()
+    got = np.asarray(got).astype(np.complex128).ravel()
+    return float(np.linalg.norm(ref - got) / np.linalg.norm(ref))
+
+
+def nodes(n, M, seed, kind="uniform"):
+    rng = np.random.default_rng(seed)
+    if kind == "dense":  # everything in one cell of one tile
+        return rng.random((M, 3)) * 0.9 / n[0] + 0.1 / n[0]
+    if kind == "clustered":
+        c = rng.random((4, 3)) - 0.5
+        x = c[rng.integers(0, 4, M)] + 0.03 * rng.standard_normal((M, 3))
+        return (x + 0.5) % 1.0 - 0.5
+    x = rng.random((M, 3)) - 0.5
+    if kind == "edges":
+        k = max(1, M // 8)
+        x[:k] = rng.integers(-n[0] // 2, n[0] // 2, size=(k, 3)) / np.array(n)  # aligned: wide stencils
+        x[k:2 * k, 0] = -0.5
+        x[2 * k:3 * k, -1] = np.nextafter(0.5, 0.0)
+        x[3 * k:4 * k, 1] = rng.integers(-n[1] // 2, n[1] // 2, size=k) / n[1]  # wide in one dim only
+    return x
+
+
+def plan(N, n, x, monkeypatch, teams=None):
+    monkeypatch.setenv("NFFTK_TILE", "8")
+    if teams:
+        monkeypatch.setenv("NFFTK_RES_TEAMS", str(teams))
+    p = nf.Plan(N, x.shape[0], n=n, m=M4)
+    p.x = x
+    p.precompute()
+    assert p.tile == (8, 8, 8) and p.gridding == "residue"
+    return p
+
+
+def check(p, N, n, x, oracle, reps=1):
+    rng = np.random.default_rng(7)
+    fh = rng.standard_normal(int(np.prod(N))) + 1j * rng.standard_normal(int(np.prod(N)))
+    fs = rng.standard_normal(x.shape[0]) + 1j * rng.standard_normal(x.shape[0])
+    rt = oracle.trafo(N, n, M4, x, fh)
+    ra = oracle.adjoint(N, n, M4, x, fs)
+    for _ in range(reps):
+        assert e2(rt, p.trafo(fh)) < 1e-12
+        assert e2(ra, p.adjoint(fs)) < 1e-12
+
+
+@pytest.mark.parametrize("n1", [24, 32, 20, 36, 18])
+def test_residue_grids(n1, oracle, monkeypatch):
+    """n a multiple of the tile edge, and not (the last tile of a dim is partial)."""
+    N, n = (8, 8, 8), (n1, n1, n1)
+    x = nodes(n, 6000, seed=n1, kind="edges")
+    p = plan(N, n, x, monkeypatch)
+    assert p.wide_nodes >= 6000 // 8
+    check(p, N, n, x, oracle)
+
+
+def test_residue_anisotropic(oracle, monkeypatch):
+    N, n = (8, 16, 12), (24, 40, 32)
+    x = nodes(n, 9000, seed=3)
+    check(plan(N, n, x, monkeypatch), N, n, x, oracle)
+
+
+@pytest.mark.parametrize("teams", [3, 4])
+@pytest.mark.parametrize("kind", ["uniform", "clustered", "dense"])
+def test_residue_node_sets(kind, teams, oracle, monkeypatch):
+    N, n = (16, 16, 16), (32, 32, 32)
+    x = nodes(n, 20000 if kind != "dense" else 5000, seed=11, kind=kind)
+    p = plan(N, n, x, monkeypatch, teams=teams)
+    check(p, N, n, x, oracle, reps=2)
+
+
+@pytest.mark.parametrize("M", [1, 3, 4, 5, 15, 16, 17, 63, 64, 65, 97])
+def test_residue_batch_boundaries(M, oracle, monkeypatch):
+    N, n = (8, 8, 8), (24, 24, 24)
+    x = nodes(n, M, seed=M)
+    check(plan(N, n, x, monkeypatch), N, n, x, oracle)
+
+
+def test_residue_all_nodes_aligned(oracle, monkeypatch):
+    """Every stencil 2m+1 wide: the residue kernels skip every node and
+    k_wide_nodes does the whole transform."""
+    N, n = (8, 8, 8), (24, 24, 24)
+    rng = np.random.default_rng(5)
+    x = rng.integers(-12, 12, size=(500, 3)) / 24.0
+    p = plan(N, n, x, monkeypatch)
+    assert p.wide_nodes == 500
+    check(p, N, n, x, oracle)
+
+
+def test_residue_matches_row_kernels(oracle, monkeypatch):
+    """Same plan parameters through the row-per-thread pipelined kernels
+    (NFFTK_NO_RES): the two B / B^H implementations agree to rounding."""
+    N, n = (16, 16, 16), (32, 32, 32)
+    x = nodes(n, 30000, seed=21, kind="edges")
+    rng = np.random.default_rng(9)
+    fh = rng.standard_normal(16 ** 3) + 1j * rng.standard_normal(16 ** 3)
+    fs = rng.standard_normal(30000) + 1j * rng.standard_normal(30000)
+    p = plan(N, n, x, monkeypatch)
+    monkeypatch.setenv("NFFTK_NO_RES", "1")
+    q = nf.Plan(N, 30000, n=n, m=M4)
+    q.x = x
+    q.precompute()
+    monkeypatch.delenv("NFFTK_NO_RES")
+    assert q.gridding == "pipe"
+    assert e2(q.trafo(fh), p.trafo(fh)) < 1e-13
+    assert e2(q.adjoint(fs), p.adjoint(fs)) < 1e-13

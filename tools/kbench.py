@@ -29,7 +29,7 @@ def main():
     name = sys.argv[1]
     single = "--single" in sys.argv
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 10
-    w = wl.CONFIGS[name]
+    w = wl.lookup(name)
     prec = "single" if single else "double"
     cdt = torch.complex64 if single else torch.complex128
     p = nf.Plan(w.N, w.M, n=w.n, m=w.m, precision=prec)

@@ -18,7 +18,7 @@ def main():
     if "--psi" in sys.argv:
         psi = sys.argv[sys.argv.index("--psi") + 1]
     prec = "single" if "--single" in sys.argv else "double"
-    w = wl.CONFIGS[name]
+    w = wl.lookup(name)
     p = nf.Plan(w.N, w.M, n=w.n, m=w.m, precision=prec)
     if psi:
         p.set_psi_policy(nf.MODE_DIRECT if psi == "direct" else nf.MODE_TENSOR)
