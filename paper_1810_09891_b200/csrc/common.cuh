@@ -118,7 +118,7 @@ struct Geom {
   double lut_step[MAX_D];
   const double* psi;      // M * psi_row(d, 2m+1) in sorted order (MODE_TENSOR)
   const int4* rec;        // M per-node stencil records, sorted order
-  int psi_pad;            // d = 3 pipelined PRE_PSI layout: 0 none (stencil rows), 1 halo-indexed, 2 sten3 blocks, 3 residue rows (RES_PR)
+  int psi_pad;            // d = 3 pipelined PRE_PSI layout: 0 none (stencil rows), 1 halo-indexed, 2 sten3 blocks
   int pr;                 // PRE_PSI row stride (doubles)
   int64_t M;
   int nt_interp;          // threads per interp CTA
@@ -129,21 +129,19 @@ struct Geom {
   int dense_flush;        // pipelined c128 spread reduces into the dense grid (periodic wrap per row), no fold
   int psi_f32;            // PRE_PSI rows stored as fp32 (c64 plans on the pipelined geometries); psi then points at floats
   unsigned* sched;        // plan-owned ticket counters for persistent kernels (SCHED_* slots; null: static order)
-  int res;                // residue-owned d = 3 kernels (residue.cu): node order and records built for them
+  int res;                // residue-owned d = 3 spread (residue.cu): node order and records built for it
   int nwide;              // res: nodes with a 2m+1 wide stencil in some dim (k_wide_nodes)
   const unsigned* rrec;   // res: 4-byte node records, sorted order (RES_* bits)
 };
 
-// Residue-owned kernels (residue.cu): d = 3, m = 4, 8^3 tiles.  A regular node
+// Residue-owned spread (residue.cu): d = 3, m = 4, 8^3 tiles.  A regular node
 // (stencil 2m wide in every dim) touches halo cells h .. h + 7, h = its cell
 // inside the tile, of the 15^3 halo starting at slot tile * 8 - (m - 1).
 constexpr int RES_M = 4;
 constexpr int RES_W = 2 * RES_M;        // stencil width of a regular node
 constexpr int RES_H = 8 + RES_W - 1;    // halo edge
-constexpr int RES_PR = 3 * RES_W;       // PRE_PSI row (Geom::psi_pad = 3): [last dim | dim 0 | dim 1] x 2m factors
 // record: h0 | h1 << 3 | h2 << 6 | regular << 9
 constexpr unsigned RES_REGULAR = 1u << 9;
-constexpr unsigned RES_KEY = RES_REGULAR | 63u;   // (h0, h1) run of a regular node
 
 // Dynamic subproblem order for the persistent gridding kernels: CTA b starts at
 // subproblem b, then draws tickets gridDim.x + t from a counter, so CTAs that

@@ -2150,10 +2150,6 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
 void launch_interp(bool single, const void* tmap, const void* gp, void* f, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
-  if (!single && res_ok(g)) {  // tmap: the plan's 15^3-box map
-    launch_interp_res(tmap, gp, f, xs, perm, subs, nsubs, g, s);
-    return;
-  }
   const CUtensorMap* tm = (const CUtensorMap*)tmap;
   if (single) NFFTK_DISPATCH_DM(interp_go, float, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);
   else NFFTK_DISPATCH_DM(interp_go, double, tm, gp, f, nullptr, xs, perm, subs, nsubs, g, s);

@@ -75,10 +75,10 @@ __global__ void k_bin_keys(const double* __restrict__ x, int64_t M, Geom g,
       lc[dim] = (uint32_t)(s - (int64_t)tcoord * g.T[dim]);
     }
     if (g.res) {
-      // residue kernels: runs of equal dim-1 cell, dim 0 in serpentine order
-      // inside them (a lane's row changes when the dim-0 / dim-1 cell passes
-      // its residue: residue.cu), last dim least significant
-      local = (lc[1] * 8 + ((lc[1] & 1) ? 7 - lc[0] : lc[0])) * 8 + lc[2];
+      // residue spread (residue.cu): ascending dim-0 cell (a lane changes rows
+      // once per tile), runs of equal (dim-0, last-dim) cell inside it (one
+      // unrolled FMA body per run), dim 1 least significant
+      local = (lc[0] * 8 + lc[2]) * 8 + lc[1];
     } else {
       for (int dim = g.d - 1; dim >= 0; --dim) local = local * g.T[dim] + lc[dim];
     }
@@ -150,11 +150,6 @@ __global__ void k_build_psi(const double* __restrict__ xs, int64_t M, Geom g,
       t = r - blk * (K + 1);
       dim = blk == 0 ? g.d - 1 : (blk == 1 ? 0 : (blk == 2 ? 1 : g.d));
       if (t >= K) dim = g.d;  // the block's zero / row padding
-    } else if (g.psi_pad == 3) {
-      // residue rows: blocks of 2m -- last dim, dim 0, dim 1 (common.cuh RES_PR)
-      const int blk = r / (K - 1);
-      t = r - blk * (K - 1);
-      dim = blk == 0 ? g.d - 1 : (blk == 1 ? 0 : (blk == 2 ? 1 : g.d));
     } else {
       dim = r / K;
       t = r - dim * K;
@@ -220,14 +215,10 @@ __global__ void __launch_bounds__(256) k_build_psi_tile(const double* __restrict
     } else if (g.psi_pad == 2) {
       // sten3 blocks: last dim, dim 0, dim 1 (common.cuh)
       pos = dim == g.d - 1 ? STEN3_OW2 : (dim == 0 ? sten3_ow0(K) : sten3_ow1(K));
-    } else if (g.psi_pad == 3) {
-      // residue rows: blocks of 2m factors (a wide node's last factor is dropped;
-      // k_wide_nodes evaluates those nodes directly)
-      pos = dim == g.d - 1 ? 0 : (dim == 0 ? K - 1 : 2 * (K - 1));
     }
     slo[nd] = st.lo;
     spos[nd] = pos;
-    swid[nd] = g.psi_pad == 3 ? min(st.width, K - 1) : st.width;
+    swid[nd] = st.width;
   }
   __syncthreads();
   const int items = nn * g.d * K;

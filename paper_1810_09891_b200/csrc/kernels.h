@@ -39,13 +39,12 @@ bool pipe_geometry(const Geom& g);
 bool spread_dense_ok(const Geom& g, int elem_bytes);
 void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, unsigned* rrec, unsigned* nwide,
                 cudaStream_t s);
-// residue-owned d = 3 kernels (residue.cu)
+// residue-owned d = 3 spread (residue.cu)
 bool res_geometry(const Geom& g, bool single);
 bool res_ok(const Geom& g);
 void launch_spread_res(void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
                        const Geom& g, cudaStream_t s);
-void launch_interp_res(const void* tmap, const void* grid, void* f, const double* xs, const int* perm,
-                       const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
+
 void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaStream_t s);
 void psi_reference(const double* x_dev, int64_t M, const Geom& g, double* psi, double* vals, int64_t* idx,
                    int64_t* counts, cudaStream_t s);

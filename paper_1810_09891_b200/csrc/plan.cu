@@ -536,15 +536,6 @@ static void build_tensor_map(Plan* p) {
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS) fail(EK_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
-  if (g.res) {
-    // residue interp: the 15^3 halo of regular nodes (residue.cu)
-    for (int i = 0; i < 3; ++i) box[i] = (cuuint32_t)RES_H;
-    box[0] *= scale;
-    res = encode((CUtensorMap*)p->tmap_res, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p->gp, dims, strides, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (res != CUDA_SUCCESS) fail(EK_CUDA, "cuTensorMapEncodeTiled (residue box) failed (" + std::to_string((int)res) + ")");
-  }
   p->tmap_ready = true;
 }
 
@@ -636,9 +627,7 @@ void plan_precompute(Plan* p, cudaStream_t s) {
   if (mode == MODE_TENSOR) {
     const int K = 2 * p->m + 1;
     p->geom.psi_pad = p->d == 3 && pipe_geometry(p->geom) ? (pipe_sten3(p->single, p->m) ? 2 : 1) : 0;
-    if (p->geom.res) p->geom.psi_pad = 3;
-    const int pad_count = p->geom.psi_pad == 3 ? RES_PR
-                          : p->geom.psi_pad == 2 ? sten3_count(K) : psi_row_halo(p->d, p->geom.H, K);
+    const int pad_count = p->geom.psi_pad == 2 ? sten3_count(K) : psi_row_halo(p->d, p->geom.H, K);
     p->geom.pr = p->geom.psi_pad ? psi_row_pad<double>(pad_count) : psi_row(p->d, K);
     // c64 plans on the pipelined geometries (only the pipelined kernels read
     // the table there) keep fp32 factor rows: half the bytes, no per-FMA
@@ -699,8 +688,7 @@ void plan_interp_device(Plan* p, void* f, cudaStream_t s) {
   NFFTK_CUDA(cudaSetDevice(p->device));
   { PhaseScope ps(p, PH_PAD, s); launch_pad(p->single, p->grid, p->gp, p->pq, s); }
   { PhaseScope ps(p, PH_INTERP, s);
-    launch_interp(p->single, res_ok(p->geom) ? p->tmap_res : p->tmap, p->gp, f, p->xs, p->perm, p->subs,
-                  p->nsubs, p->geom, s); }
+    launch_interp(p->single, p->tmap, p->gp, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
   NFFTK_CUDA(cudaGetLastError());
   count_evals(p);
 }

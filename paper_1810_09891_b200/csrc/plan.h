@@ -66,7 +66,6 @@ struct Plan {
   size_t gp_bytes = 0;
   PadGeom pq{};
   alignas(64) unsigned char tmap[128];  // CUtensorMap of gp (halo boxes)
-  alignas(64) unsigned char tmap_res[128];  // CUtensorMap of gp with 15^3 boxes (residue interp)
   bool tmap_ready = false;
   void* fhat_dev = nullptr;
   void* f_dev = nullptr;

@@ -1,33 +1,28 @@
-// Residue-owned gridding kernels (sm_100a) for d = 3, m = 4, 8^3 tiles:
-//   B^H (spread): g[l mod n] += f_j prod_i psi_i(x_ji - l_i / n_i)   kernels.py:209-401
-//   B   (interp): f_j = sum_l g[l mod n] prod_i psi_i(...)           kernels.py:122-197
+// Residue-owned spread kernel (sm_100a) for d = 3, m = 4, 8^3 tiles:
+//   B^H: g[l mod n] += f_j prod_i psi_i(x_ji - l_i / n_i)      kernels.py:209-401
 //
 // A regular node (stencil 2m = 8 cells wide in every dim) of an 8^3 tile
-// touches the halo cells h_i .. h_i + 7 with h_i = its cell inside the tile,
-// so the cells it touches lie in a 15^3 halo and cover every residue class
-// (a mod 8, b mod 8) of the leading two dims exactly once.  A TEAM of 64
-// lanes therefore owns the halo by residue: lane (ra, rb) holds the halo row
-// (a, b, 0..14) with a = ra or ra + 8, b = rb or rb + 8 -- whichever lies in
-// the current node's stencil -- as 15 complex register accumulators, and
-// every lane does useful FMAs for every node (the row-per-thread kernels in
-// gridding.cu keep 17^2 rows on 289 threads of which 64 work per node).
-//   * Nodes of a tile arrive sorted by (h_1, then h_0 in serpentine order)
-//     (k_bin_keys), so the row a lane needs changes rarely: when h_0 passes
-//     ra (8 lanes of one warp, ~56 times per tile) or h_1 passes rb (7 times).
-//     The leaving row goes to the lane's own slot of the team's shared-memory
-//     halo, the entering one comes from there (zero if never written).
-//   * Row stride 15 cells (240 B): the 8 lanes of a quarter warp (rb = 0..7)
-//     hit 8 different 16-byte bank groups; no other lane touches a lane's
-//     rows, so there are no atomics and no barriers in the spread.
-//   * Node batches (PRE_PSI rows of 3 x 8 factors, 4-byte stencil records,
-//     samples / output indices) arrive by TMA bulk copies on a per-team
-//     mbarrier ring; the spread flushes each written row with one TMA bulk
-//     fp64 reduction into the dense grid (periodic wrap per row); the interp
-//     loads the 15^3 halo with one TMA tensor copy per tile.
-//   * One persistent CTA per SM holds NT independent teams (own halo, ring,
-//     barriers and subproblem tickets).
+// touches the halo cells h_i .. h_i + 7, h_i = its cell inside the tile, of
+// the 15^3 halo that starts at slot tile * 8 - (m - 1).  Along dim 0 those
+// eight cells cover every residue class a mod 8 exactly once, so a CTA of
+// 15 x 8 lanes owns the halo rows by (b, a mod 8): lane (b, ra) holds the
+// row (a, b, 0..14) with a = ra while the nodes' dim-0 start h_0 is <= ra,
+// a = ra + 8 afterwards, as 15 complex register accumulators.
+//   * Every lane of a warp whose four b values meet the node's dim-1 window
+//     has a row inside the node's dim-0 stencil: 2.75 warps of 4 work per
+//     node at 8/11 useful lanes, against 5.8 of 10 at 44% for the
+//     row-per-thread kernel (gridding.cu k_spread_pipe, 17^2 rows on 289
+//     threads) -- half the per-node instruction stream.
+//   * Nodes of a tile arrive sorted by (h_0, h_2, h_1) (k_bin_keys): a lane
+//     changes rows once per tile (when h_0 passes ra: the finished row leaves
+//     by a TMA bulk fp64 reduction straight away), and the nodes of a run of
+//     equal (h_0, h_2) share the unrolled FMA body with static register
+//     indices (one switch per run) and the lane's dim-0 factor offset.
+//   * One shared-memory row per lane stages the reductions (28.8 KB), so five
+//     128-thread CTAs fit an SM; node batches (sten3 PRE_PSI rows, 4-byte
+//     records, sorted samples) arrive by TMA bulk copies on an mbarrier ring.
 // Nodes with a 2m+1 wide stencil in some dim (n x an exact integer) are
-// skipped here and handled by k_wide_* (direct window evaluation, atomics).
+// skipped here and spread by k_wide_nodes (direct window evaluation, atomics).
 #include <cuda.h>
 
 #include <algorithm>
@@ -39,32 +34,61 @@
 
 namespace nfftk {
 
-struct ResMeta {
+struct AresMeta {
   int tile;  // tile of this batch
   int nb;    // nodes (< 0: end of work)
   int last;  // last batch of its subproblem
-  int off;   // offset of the 4-byte arrays inside the stage (16-byte bulk copies)
+  int off;   // offset of the records inside the stage (16-byte bulk copies)
 };
 
-template <typename R, int NT_, int NB_, int S_, bool INTERP>
-struct ResCfg {
-  static constexpr int NT = NT_, NB = NB_, S = S_;
+template <typename R, int NB_, int S_>
+struct AresCfg {
+  static constexpr int NB = NB_, S = S_;
+  static constexpr int K = 2 * RES_M + 1;
   static constexpr int ELEM = 2 * (int)sizeof(R);
-  static constexpr int FA = 16 / ELEM;                     // samples per 16 bytes
-  static constexpr int ROW = RES_H * ELEM;                 // one halo row, bytes
+  static constexpr int FA = 16 / ELEM;                    // samples per 16 bytes
+  static constexpr int PR = psi_row_pad<R>(sten3_count(K));  // sten3 PRE_PSI row (common.cuh)
+  static constexpr int OW0 = sten3_ow0(K), OW1 = sten3_ow1(K);
+  static constexpr int THREADS = 128;                     // 16 x 8 lanes, b = 15 idle
+  static constexpr int ROWS = RES_H * 8;
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
-  static constexpr size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
-  static constexpr size_t HALO = al128((size_t)RES_H * RES_H * ROW);
-  static constexpr size_t W_BYTES = al(sizeof(R) * NB * RES_PR);
+  static constexpr size_t ROWS_BYTES = al((size_t)ROWS * RES_H * ELEM);
+  static constexpr size_t W_BYTES = al(sizeof(R) * NB * PR);
   static constexpr size_t R_BYTES = al(4 * (size_t)(NB + 4));
-  static constexpr size_t X_BYTES = INTERP ? al(4 * (size_t)(NB + 4)) : al((size_t)ELEM * (NB + FA));
-  static constexpr size_t SB = W_BYTES + R_BYTES + X_BYTES;
-  static constexpr size_t CTL = al(8 * (2 * (size_t)S + 2) + sizeof(ResMeta) * S + 32);
-  static constexpr size_t PART = INTERP ? (size_t)S * 2 * NB * ELEM : 0;  // interp: per-warp node sums
-  static constexpr size_t TEAM_BYTES = al128(HALO + S * SB + CTL + PART);
-  static constexpr size_t SMEM = NT * TEAM_BYTES;
-  static constexpr int THREADS = NT * 64;
+  static constexpr size_t F_BYTES = al((size_t)ELEM * (NB + FA));
+  static constexpr size_t SB = W_BYTES + R_BYTES + F_BYTES;
+  static constexpr size_t RING_OFF = ROWS_BYTES;
+  static constexpr size_t CTL_OFF = RING_OFF + S * SB;
+  static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 32);
 };
+
+#define NFFTK_ARES_NODE(H)                                                                 \
+  {                                                                                        \
+    m2 &= m2 - 1;                                                                          \
+    const int jn = m2 ? __ffs(m2) - 1 : jj;                                                \
+    const unsigned rn = rs[jn]; /* next node's record, under this node's FMAs */           \
+    const R* pw = ws + jj * PR;                                                            \
+    const R s = pw[offa] * pw[P::OW1 + min((unsigned)(b - b0), (unsigned)K)];              \
+    const C f = fv[jj];                                                                    \
+    const R cr = f.x * s, ci = f.y * s;                                                    \
+    R w2[RES_W];                                                                           \
+    load8<R>(pw, w2);                                                                      \
+    _Pragma("unroll") for (int t = 0; t < RES_W; ++t) {                                    \
+      accr[H + t] = fma(cr, w2[t], accr[H + t]);                                           \
+      acci[H + t] = fma(ci, w2[t], acci[H + t]);                                           \
+    }                                                                                      \
+    jj = jn;                                                                               \
+    b0 = (int)((rn >> 3) & 7);                                                             \
+  }
+#define NFFTK_ARES_CASE(H)             \
+  case H: {                            \
+    unsigned m2 = run;                 \
+    int jj = __ffs(m2) - 1;            \
+    int b0 = (int)((rs[jj] >> 3) & 7); \
+    do {                               \
+      NFFTK_ARES_NODE(H)               \
+    } while (m2);                      \
+  } break;
 
 template <typename R>
 __device__ __forceinline__ void load8(const R* w, R* o) {
@@ -89,34 +113,26 @@ __device__ __forceinline__ void load8(const R* w, R* o) {
   }
 }
 
-__device__ __forceinline__ void team_sync(int team) {
-  asm volatile("bar.sync %0, 64;\n" ::"r"(team + 1) : "memory");
-}
-
-// Team ticket order: team t of CTA b starts at subproblem b * NT + t, then
-// draws nteams + ticket from the plan's counter (common.cuh next_sub, per team).
-__device__ __forceinline__ int res_next_sub(const Geom& g, int slot, int cur, int nteams) {
-  if (!g.sched) return cur + nteams;
-  return nteams + (int)atomicAdd(g.sched + slot, 1u);
-}
-__device__ __forceinline__ void res_sched_done(const Geom& g, int slot, int nteams) {
-  if (!g.sched) return;
-  __threadfence();
-  if (atomicAdd(g.sched + slot + 1, 1u) == (unsigned)nteams - 1) {
-    g.sched[slot] = 0;
-    g.sched[slot + 1] = 0;
-    __threadfence();
-  }
-}
-
-// Per-team producer of the node ring (one thread): stage pk goes to slot pk % S.
-template <typename P, typename R, bool INTERP>
-struct ResProducer {
-  unsigned char* ring;
-  unsigned long long *full, *empty;
-  ResMeta* meta;
-  int* pst;  // 0: sub, 1: base, 2: end, 3: tile, 4: pk
-  __device__ __forceinline__ void load_sub(const int4* subs, int s, int nsubs) {
+template <typename R, int NB, int S, int BLOCKS>
+__global__ void __launch_bounds__(128, BLOCKS)
+k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted,
+             const R* __restrict__ psi, const unsigned* __restrict__ rrec,
+             const int4* __restrict__ subs, int nsubs, Geom g) {
+  using C = cplx_t<R>;
+  using P = AresCfg<R, NB, S>;
+  constexpr int K = P::K, PR = P::PR;
+  static_assert(NB <= 32, "one ballot per batch");
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL_OFF);
+  unsigned long long* empty = full + S;
+  AresMeta* meta = reinterpret_cast<AresMeta*>(empty + S);
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = threadIdx.x >> 3, ra = threadIdx.x & 7;
+  const bool owner = b < RES_H;
+  const int wb_lo = warp * 4, wb_hi = warp * 4 + 3;
+  C* const myrow = reinterpret_cast<C*>(smem) + (size_t)(owner ? threadIdx.x : 0) * RES_H;
+  auto load_sub = [&](int s) {
     pst[0] = s;
     if (s < nsubs) {
       const int4 sp = subs[s];
@@ -124,16 +140,12 @@ struct ResProducer {
       pst[2] = sp.y + sp.z;
       pst[3] = sp.x;
     }
-  }
-  template <typename F>
-  __device__ __forceinline__ void produce(const R* psi, const unsigned* rrec, const void* xarr,
-                                          const int4* subs, int nsubs, const Geom& g, int slot_id,
-                                          int nteams, F&& on_new_sub) {
-    constexpr int S = P::S, NB = P::NB;
+  };
+  auto produce = [&]() {
     const int pk = pst[4];
     const int slot = pk % S;
     if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
-    ResMeta* mt = meta + slot;
+    AresMeta* mt = meta + slot;
     pst[4] = pk + 1;
     if (pst[0] >= nsubs) {
       mt->nb = -1;
@@ -144,440 +156,125 @@ struct ResProducer {
     const int nb = min(NB, pend - pbase);
     const int off = pbase & 3;
     const int rcnt = (nb + off + 3) & ~3;
+    constexpr int FA = P::FA;
+    const int foff = pbase & (FA - 1);
     mt->tile = pst[3];
     mt->nb = nb;
     mt->last = pbase + nb >= pend;
     mt->off = off;
-    unsigned char* st = ring + slot * P::SB;
-    const unsigned wb = (unsigned)(sizeof(R) * RES_PR) * nb, rb = 4u * rcnt;
-    unsigned xb;
-    const unsigned char* xsrc;
-    if constexpr (INTERP) {
-      xb = rb;
-      xsrc = reinterpret_cast<const unsigned char*>(reinterpret_cast<const int*>(xarr) + (pbase - off));
-    } else {
-      constexpr int FA = P::FA;
-      const int foff = pbase & (FA - 1);
-      xb = (unsigned)P::ELEM * ((nb + foff + FA - 1) & ~(FA - 1));
-      xsrc = reinterpret_cast<const unsigned char*>(xarr) + (size_t)P::ELEM * (pbase - foff);
-    }
-    mbar_expect_tx(full + slot, wb + rb + xb);
-    bulk_g2s(st, psi + (int64_t)pbase * RES_PR, wb, full + slot);
+    unsigned char* st = smem + P::RING_OFF + slot * P::SB;
+    const unsigned wb = (unsigned)(sizeof(R) * PR) * nb, rb = 4u * rcnt,
+                   fb = (unsigned)P::ELEM * ((nb + foff + FA - 1) & ~(FA - 1));
+    mbar_expect_tx(full + slot, wb + rb + fb);
+    bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot);
-    bulk_g2s(st + P::W_BYTES + P::R_BYTES, xsrc, xb, full + slot);
-    if (pbase + nb < pend) {
-      pst[1] = pbase + nb;
-    } else {
-      load_sub(subs, res_next_sub(g, slot_id, pst[0], nteams), nsubs);
-      if (pst[0] < nsubs) on_new_sub(pst[1], pst[2] - pst[1], pst[3]);
-    }
-  }
-};
-
-// ------------------------------------------------------------------ B^H
-// One node's operands for this lane, loaded one node ahead of its FMAs: the
-// record, the lane's two leading-dim factors, the sample and the 2m last-dim
-// factors (a team has two warps per SM sub-partition at most, so the load
-// latency has to be covered inside the warp).
-template <typename R>
-struct ResNode {
-  unsigned r;
-  R wa, wb;
-  cplx_t<R> f;
-  R w2[RES_W];
-};
-
-#define NFFTK_RES_SPREAD_CASE(k)                          \
-  case k:                                                 \
-    _Pragma("unroll") for (int t = 0; t < RES_W; ++t) {   \
-      accr[k + t] = fma(vr, w2[u][t], accr[k + t]);       \
-      acci[k + t] = fma(vi, w2[u][t], acci[k + t]);       \
-    }                                                     \
-    break;
-
-template <typename R, int NT, int NB, int S>
-__global__ void __launch_bounds__(NT * 64, 1)
-k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted,
-             const R* __restrict__ psi, const unsigned* __restrict__ rrec,
-             const int4* __restrict__ subs, int nsubs, Geom g) {
-  using C = cplx_t<R>;
-  using P = ResCfg<R, NT, NB, S, false>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int team = threadIdx.x >> 6, tt = threadIdx.x & 63, lane = threadIdx.x & 31;
-  const int ra = tt >> 3, rb = tt & 7;
-  unsigned char* tb = smem + team * P::TEAM_BYTES;
-  C* halo = reinterpret_cast<C*>(tb);
-  ResProducer<P, R, false> pr;
-  pr.ring = tb + P::HALO;
-  pr.full = reinterpret_cast<unsigned long long*>(pr.ring + S * P::SB);
-  pr.empty = pr.full + S;
-  pr.meta = reinterpret_cast<ResMeta*>(pr.empty + S + 2);
-  pr.pst = reinterpret_cast<int*>(pr.meta + S);
-  const int nteams = (int)gridDim.x * NT;
-  // the next subproblem's node data is pulled into L2 when the producer draws it
-  auto prefetch = [&](int base, int cnt, int) {
-    l2_prefetch(psi + (int64_t)base * RES_PR, (unsigned)(sizeof(R) * RES_PR) * (unsigned)cnt);
-    l2_prefetch(fsorted + (base & ~1), (unsigned)sizeof(C) * (unsigned)((cnt + 2) & ~1));
-    l2_prefetch(rrec + (base & ~3), 4u * (unsigned)((cnt + 6) & ~3));
+    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (pbase + nb < pend) pst[1] = pbase + nb;
+    else load_sub(next_sub(g, SCHED_SPREAD3, pst[0]));
   };
-  if (tt == 0) {
+  if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(pr.full + i, 1);
-      mbar_init(pr.empty + i, 2);
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, P::THREADS / 32);
     }
-    pr.pst[4] = 0;
-    pr.load_sub(subs, (int)blockIdx.x * NT + team, nsubs);
+    pst[4] = 0;
+    load_sub((int)blockIdx.x);
   }
-  // the ring starts zeroed: the node loop reads whole groups of four, and a
-  // batch's unused entries must hold finite factors (they are multiplied by 0)
-  for (int i = tt; i < (int)(S * P::SB / 16); i += 64) reinterpret_cast<int4*>(pr.ring)[i] = make_int4(0, 0, 0, 0);
-  fence_proxy_async_smem();
-  team_sync(team);
-  if (tt == 0)
-    for (int i = 0; i < S; ++i) pr.produce(psi, rrec, fsorted, subs, nsubs, g, SCHED_SPREAD3, nteams, prefetch);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < S - 1; ++i) produce();
 
   R accr[RES_H], acci[RES_H];
 #pragma unroll
   for (int c = 0; c < RES_H; ++c) accr[c] = acci[c] = 0;
-  unsigned touched = 0;  // images of this lane written to the shared halo
-  int cia = 0, cib = 0;  // image in registers: row (ra + 8 cia, rb + 8 cib)
-  bool written = false;  // the image in registers has been entered by a node of this subproblem
-  auto row_of = [&](int ia, int ib) { return halo + ((ra + 8 * ia) * RES_H + rb + 8 * ib) * RES_H; };
-  auto store_row = [&]() {
-    // the lane's previous bulk reductions have finished reading its rows
-    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    C* rw = row_of(cia, cib);
+  // stage this lane's registers in its shared row and reduce them into the
+  // dense grid row (a, b) of the tile (halo cell = slot tile * 8 - (m - 1) + cell)
+  auto flush_row = [&](int tile, int a) {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // the row's previous reduction has read it
 #pragma unroll
     for (int c = 0; c < RES_H; ++c) {
       C v;
       v.x = accr[c];
       v.y = acci[c];
-      rw[c] = v;
+      myrow[c] = v;
+      accr[c] = acci[c] = 0;
     }
-    touched |= 1u << (cia * 2 + cib);
+    fence_proxy_async_smem();
+    int tc[3];
+    tile_of<3>(g, tile, tc);
+    int ad = tc[0] * 8 - (RES_M - 1) + a, bd = tc[1] * 8 - (RES_M - 1) + b;
+    ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+    bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
+    bulk_red_row_wrapped<R>(grid, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - (RES_M - 1), g.n[2], myrow,
+                            RES_H);
+    asm volatile("cp.async.bulk.commit_group;\n" ::);
   };
   int k = 0;
-  for (;;) {  // subproblems of this team
+  for (;;) {  // subproblems of this CTA
     int tile = -1;
-    unsigned cur_key = ~0u;  // no record has this key: the first node of a subproblem always takes the run path
+    bool upper = false;    // this lane holds row ra + 8 (the nodes' dim-0 start has passed ra)
+    bool touched = false;  // a node met this warp's rows since its registers were zeroed
     for (;; ++k) {  // batches of the subproblem
       const int slot = k % S;
-      // refill the slot consumed one batch ago (both warps are past it)
-      if (tt == 0 && k > 0) pr.produce(psi, rrec, fsorted, subs, nsubs, g, SCHED_SPREAD3, nteams, prefetch);
-      mbar_wait(pr.full + slot, (k / S) & 1);
-      const ResMeta mt = pr.meta[slot];
+      mbar_wait(full + slot, (k / S) & 1);
+      const AresMeta mt = meta[slot];
       if (mt.nb < 0) break;
       tile = mt.tile;
-      const unsigned char* st = pr.ring + slot * P::SB;
-      const R* pw = reinterpret_cast<const R*>(st);
+      const unsigned char* st = smem + P::RING_OFF + slot * P::SB;
+      const R* ws = reinterpret_cast<const R*>(st);
       const unsigned* rs = reinterpret_cast<const unsigned*>(st + P::W_BYTES) + mt.off;
-      const C* pf = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (P::FA > 1 ? (mt.off & (P::FA - 1)) : 0);
-      // four nodes at a time: all their operands are requested before the
-      // first FMA (a team has at most two warps per SM sub-partition, so the
-      // shared-memory latency has to be covered inside the warp)
-      for (int j0 = 0; j0 < mt.nb; j0 += 4) {
-        unsigned r[4];
-        R wa[4], wb[4], w2[4][RES_W];
-        C f[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int jj = j0 + u;
-          // past the batch: a record without RES_REGULAR (factor product zeroed below)
-          r[u] = jj < mt.nb ? rs[jj] : 0u;
-          const R* w = pw + jj * RES_PR;
-          wa[u] = w[RES_W + ((ra - (int)r[u]) & 7)];
-          wb[u] = w[2 * RES_W + ((rb - (int)(r[u] >> 3)) & 7)];
-          f[u] = pf[jj];
-          load8<R>(w, w2[u]);
+      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (P::FA > 1 ? (mt.off & (P::FA - 1)) : 0);
+      // Per-batch warp view: lane l holds node l's record; one ballot gives
+      // the regular nodes whose dim-1 window meets this warp's four b values,
+      // another the starts of runs of equal (h_0, h_2).
+      const unsigned rl = lane < mt.nb ? rs[lane] : 0u;
+      const int bl = (int)((rl >> 3) & 7);
+      unsigned mask = __ballot_sync(~0u, (rl & RES_REGULAR) && bl <= wb_hi && bl + RES_W - 1 >= wb_lo);
+      const unsigned kl = rl & 0x1c7u;
+      const unsigned kup = __shfl_up_sync(~0u, kl, 1);
+      const unsigned rstart = __ballot_sync(~0u, lane == 0 || kl != kup);
+      while (mask) {
+        const int j0 = __ffs(mask) - 1;
+        const unsigned key = __shfl_sync(~0u, kl, j0);
+        const unsigned later = rstart & ~((2u << j0) - 1u);  // run starts after j0 (2u << 31 == 0)
+        const unsigned run = later ? mask & ((later & (0u - later)) - 1u) : mask;
+        mask &= ~run;
+        const int a0 = (int)(key & 7);
+        // nodes come by ascending h_0: once it passes ra, row ra is complete
+        if (owner && !upper && ra < a0) {
+          if (touched) flush_row(tile, ra);
+          upper = true;
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          R s = wa[u] * wb[u];
-          // one test per node: a new (h0, h1) run or a wide node (its key
-          // never equals a regular node's)
-          if ((r[u] & RES_KEY) != cur_key) {
-            if (!(r[u] & RES_REGULAR)) {
-              s = 0;  // 2m+1 wide stencil: k_wide_nodes spreads it
-            } else {
-              cur_key = r[u] & RES_KEY;
-              const int nia = ra < (int)(r[u] & 7), nib = rb < (int)((r[u] >> 3) & 7);
-              if (nia != cia || nib != cib) {
-                if (written) store_row();
-                const C* rw = row_of(nia, nib);
-                if (touched & (1u << (nia * 2 + nib))) {
-#pragma unroll
-                  for (int c = 0; c < RES_H; ++c) {
-                    const C v = rw[c];
-                    accr[c] = v.x;
-                    acci[c] = v.y;
-                  }
-                } else {
-#pragma unroll
-                  for (int c = 0; c < RES_H; ++c) accr[c] = acci[c] = 0;
-                }
-                cia = nia;
-                cib = nib;
-              }
-              written = true;
-            }
-          }
-          const R vr = f[u].x * s, vi = f[u].y * s;
-          switch ((r[u] >> 6) & 7) {
-            NFFTK_RES_SPREAD_CASE(0) NFFTK_RES_SPREAD_CASE(1) NFFTK_RES_SPREAD_CASE(2) NFFTK_RES_SPREAD_CASE(3)
-            NFFTK_RES_SPREAD_CASE(4) NFFTK_RES_SPREAD_CASE(5) NFFTK_RES_SPREAD_CASE(6) NFFTK_RES_SPREAD_CASE(7)
-          }
+        touched = true;
+        const int offa = P::OW0 + ((ra - a0) & 7);
+        switch (key >> 6) {
+          NFFTK_ARES_CASE(0) NFFTK_ARES_CASE(1) NFFTK_ARES_CASE(2) NFFTK_ARES_CASE(3)
+          NFFTK_ARES_CASE(4) NFFTK_ARES_CASE(5) NFFTK_ARES_CASE(6) NFFTK_ARES_CASE(7)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(pr.empty + slot);
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (threadIdx.x == 0) produce();
       if (mt.last) {
         ++k;
         break;
       }
     }
     if (tile < 0) break;  // end of work
-    // subproblem done: every lane reduces the rows it wrote into the dense
-    // grid (halo cell (a, b, c) = slot tile * 8 - (m - 1) + (a, b, c), wrapped)
-    if (written) store_row();
-#pragma unroll
-    for (int c = 0; c < RES_H; ++c) accr[c] = acci[c] = 0;
-    written = false;
-    if (touched) {
-      fence_proxy_async_smem();
-      int tc[3];
-      tile_of<3>(g, tile, tc);
-      const int c0 = tc[2] * 8 - (g.m - 1);
-#pragma unroll
-      for (int img = 0; img < 4; ++img) {
-        if (!(touched & (1u << img))) continue;
-        const int a = ra + 8 * (img >> 1), b = rb + 8 * (img & 1);
-        int ad = tc[0] * 8 - (g.m - 1) + a, bd = tc[1] * 8 - (g.m - 1) + b;
-        ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
-        bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
-        bulk_red_row_wrapped<R>(grid, ((int64_t)ad * g.n[1] + bd) * g.n[2], c0, g.n[2],
-                                halo + (a * RES_H + b) * RES_H, RES_H);
-      }
-      asm volatile("cp.async.bulk.commit_group;\n" ::);
-      touched = 0;
-    }
+    if (owner && touched) flush_row(tile, ra + (upper ? 8 : 0));
   }
+  if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD3);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-  team_sync(team);
-  if (tt == 0) res_sched_done(g, SCHED_SPREAD3, nteams);
 }
-
-// -------------------------------------------------------------------- B
-#define NFFTK_RES_INTERP_CASE(k)                           \
-  case k:                                                  \
-    _Pragma("unroll") for (int t = 0; t < RES_W; t += 2) { \
-      p0r = fma(rowr[k + t], w2[u][t], p0r);               \
-      p0i = fma(rowi[k + t], w2[u][t], p0i);               \
-      p1r = fma(rowr[k + t + 1], w2[u][t + 1], p1r);       \
-      p1i = fma(rowi[k + t + 1], w2[u][t + 1], p1i);       \
-    }                                                      \
-    break;
-
-template <typename R, int NT, int NB, int S>
-__global__ void __launch_bounds__(NT * 64, 1)
-k_interp_res(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ fout,
-             const R* __restrict__ psi, const unsigned* __restrict__ rrec,
-             const int* __restrict__ perm, const int4* __restrict__ subs, int nsubs, Geom g) {
-  using C = cplx_t<R>;
-  using P = ResCfg<R, NT, NB, S, true>;
-  static_assert(NB % 4 == 0 && NB <= 32, "nodes are reduced four at a time, one combine lane per node");
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int team = threadIdx.x >> 6, tt = threadIdx.x & 63, lane = threadIdx.x & 31, wt = tt >> 5;
-  const int ra = tt >> 3, rb = tt & 7;
-  unsigned char* tb = smem + team * P::TEAM_BYTES;
-  const C* halo = reinterpret_cast<const C*>(tb);
-  ResProducer<P, R, true> pr;
-  pr.ring = tb + P::HALO;
-  pr.full = reinterpret_cast<unsigned long long*>(pr.ring + S * P::SB);
-  pr.empty = pr.full + S;
-  unsigned long long* hfull = pr.empty + S;
-  unsigned long long* hempty = hfull + 1;
-  pr.meta = reinterpret_cast<ResMeta*>(pr.empty + S + 2);
-  pr.pst = reinterpret_cast<int*>(pr.meta + S);
-  // per slot: the two warps' sums of the batch's nodes (combined by warp 0
-  // when both are past the batch, before the slot is refilled)
-  C* part = reinterpret_cast<C*>(pr.ring + S * P::SB + P::CTL);
-  const int nteams = (int)gridDim.x * NT;
-  constexpr int SCALE = (int)sizeof(C) / 8;
-  auto box_of = [&](int tile, int* c) {
-    int tc[3];
-    tile_of<3>(g, tile, tc);
-    // halo cell 0 = slot tile * 8 - (m - 1) = padded index tile * 8 + 1
-    c[0] = (tc[2] * 8 + 1) * SCALE;
-    c[1] = tc[1] * 8 + 1;
-    c[2] = tc[0] * 8 + 1;
-  };
-  // the next subproblem's halo and node data are pulled into L2 as soon as the producer draws it
-  auto prefetch = [&](int base, int cnt, int tile) {
-    int c[3];
-    box_of(tile, c);
-    tma_prefetch_box3(&tmap, c);
-    l2_prefetch(psi + (int64_t)base * RES_PR, (unsigned)(sizeof(R) * RES_PR) * (unsigned)cnt);
-    l2_prefetch(perm + (base & ~3), 4u * (unsigned)((cnt + 6) & ~3));
-    l2_prefetch(rrec + (base & ~3), 4u * (unsigned)((cnt + 6) & ~3));
-  };
-  if (tt == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(pr.full + i, 1);
-      mbar_init(pr.empty + i, 2);
-    }
-    mbar_init(hfull, 1);
-    mbar_init(hempty, 2);
-    pr.pst[4] = 0;
-    pr.load_sub(subs, (int)blockIdx.x * NT + team, nsubs);
-    for (int i = 0; i < S; ++i) pr.produce(psi, rrec, perm, subs, nsubs, g, SCHED_INTERP, nteams, prefetch);
-  }
-  team_sync(team);
-
-  R rowr[RES_H], rowi[RES_H];
-  unsigned cur_key = ~0u;  // no record has this key
-  int cia = -1, cib = -1;
-  // warp 0: f[perm] = both warps' sums of batch kk (its slot is about to be refilled)
-  auto combine = [&](int kk) {
-    const int slot = kk % S;
-    if (lane == 0) mbar_wait(pr.empty + slot, (kk / S) & 1);
-    __syncwarp();
-    const ResMeta mt = pr.meta[slot];
-    const unsigned char* st = pr.ring + slot * P::SB;
-    const unsigned* rs = reinterpret_cast<const unsigned*>(st + P::W_BYTES) + mt.off;
-    const int* pv = reinterpret_cast<const int*>(st + P::W_BYTES + P::R_BYTES) + mt.off;
-    if (lane < mt.nb && (rs[lane] & RES_REGULAR)) {
-      const C a = part[(slot * 2) * NB + lane], b = part[(slot * 2 + 1) * NB + lane];
-      C v;
-      v.x = a.x + b.x;
-      v.y = a.y + b.y;
-      fout[pv[lane]] = v;
-    }
-    __syncwarp();
-  };
-  int k = 0;
-  for (int it = 0;; ++it) {  // subproblems of this team
-    if (wt == 0 && k > 0) {
-      combine(k - 1);
-      if (lane == 0) pr.produce(psi, rrec, perm, subs, nsubs, g, SCHED_INTERP, nteams, prefetch);
-    }
-    mbar_wait(pr.full + k % S, (k / S) & 1);
-    const ResMeta m0 = pr.meta[k % S];
-    if (m0.nb < 0) break;
-    if (tt == 0) {
-      if (it > 0) mbar_wait(hempty, (it - 1) & 1);  // both warps are done with the previous halo
-      int c[3];
-      box_of(m0.tile, c);
-      mbar_expect_tx(hfull, (unsigned)(RES_H * RES_H * P::ROW));
-      tma_load_box<3>(tb, &tmap, c, hfull);
-    }
-    mbar_wait(hfull, it & 1);
-    cur_key = ~0u;
-    cia = cib = -1;
-    for (bool first = true;; ++k, first = false) {  // batches of the subproblem
-      const int slot = k % S;
-      if (!first && wt == 0) {
-        combine(k - 1);
-        if (lane == 0) pr.produce(psi, rrec, perm, subs, nsubs, g, SCHED_INTERP, nteams, prefetch);
-      }
-      mbar_wait(pr.full + slot, (k / S) & 1);
-      const ResMeta mt = pr.meta[slot];
-      const unsigned char* st = pr.ring + slot * P::SB;
-      const R* pw = reinterpret_cast<const R*>(st);
-      const unsigned* rs = reinterpret_cast<const unsigned*>(st + P::W_BYTES) + mt.off;
-      for (int j = 0; j < mt.nb; j += 4) {
-        // four nodes: all their operands are requested up front, then one
-        // transposing reduction -- lanes keep half of the values at each of
-        // the first two exchanges (24 shuffles for four nodes instead of 80)
-        unsigned r[4];
-        R wa[4], wb[4], w2[4][RES_W];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int jj = min(j + u, mt.nb - 1);
-          r[u] = rs[jj];
-          const R* w = pw + jj * RES_PR;
-          wa[u] = w[RES_W + ((ra - (int)r[u]) & 7)];
-          wb[u] = w[2 * RES_W + ((rb - (int)(r[u] >> 3)) & 7)];
-          load8<R>(w, w2[u]);
-        }
-        R vr[4], vi[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          R s = wa[u] * wb[u];
-          if ((r[u] & RES_KEY) != cur_key) {  // a new (h0, h1) run, or a wide node
-            if (!(r[u] & RES_REGULAR)) {
-              s = 0;  // 2m+1 wide stencil: k_wide_nodes
-            } else {
-              cur_key = r[u] & RES_KEY;
-              const int nia = ra < (int)(r[u] & 7), nib = rb < (int)((r[u] >> 3) & 7);
-              if (nia != cia || nib != cib) {
-                const C* rw = halo + ((ra + 8 * nia) * RES_H + rb + 8 * nib) * RES_H;
-#pragma unroll
-                for (int c = 0; c < RES_H; ++c) {
-                  const C v = rw[c];
-                  rowr[c] = v.x;
-                  rowi[c] = v.y;
-                }
-                cia = nia;
-                cib = nib;
-              }
-            }
-          }
-          R p0r = 0, p0i = 0, p1r = 0, p1i = 0;
-          switch ((r[u] >> 6) & 7) {
-            NFFTK_RES_INTERP_CASE(0) NFFTK_RES_INTERP_CASE(1) NFFTK_RES_INTERP_CASE(2) NFFTK_RES_INTERP_CASE(3)
-            NFFTK_RES_INTERP_CASE(4) NFFTK_RES_INTERP_CASE(5) NFFTK_RES_INTERP_CASE(6) NFFTK_RES_INTERP_CASE(7)
-          }
-          vr[u] = (p0r + p1r) * s;
-          vi[u] = (p0i + p1i) * s;
-        }
-        const bool hi16 = lane & 16, hi8 = lane & 8;
-        // xor 16: lanes 0-15 keep nodes 0, 1; lanes 16-31 keep nodes 2, 3
-        R kr0 = hi16 ? vr[2] : vr[0], ki0 = hi16 ? vi[2] : vi[0], kr1 = hi16 ? vr[3] : vr[1],
-          ki1 = hi16 ? vi[3] : vi[1];
-        kr0 += __shfl_xor_sync(0xffffffffu, hi16 ? vr[0] : vr[2], 16);
-        ki0 += __shfl_xor_sync(0xffffffffu, hi16 ? vi[0] : vi[2], 16);
-        kr1 += __shfl_xor_sync(0xffffffffu, hi16 ? vr[1] : vr[3], 16);
-        ki1 += __shfl_xor_sync(0xffffffffu, hi16 ? vi[1] : vi[3], 16);
-        // xor 8: keep one node: n = 2 * bit4 + bit3
-        R sr = hi8 ? kr1 : kr0, si = hi8 ? ki1 : ki0;
-        sr += __shfl_xor_sync(0xffffffffu, hi8 ? kr0 : kr1, 8);
-        si += __shfl_xor_sync(0xffffffffu, hi8 ? ki0 : ki1, 8);
-#pragma unroll
-        for (int o = 4; o; o >>= 1) {
-          sr += __shfl_xor_sync(0xffffffffu, sr, o);
-          si += __shfl_xor_sync(0xffffffffu, si, o);
-        }
-        if ((lane & 7) == 0) {
-          C v;
-          v.x = sr;
-          v.y = si;
-          part[(slot * 2 + wt) * NB + j + (lane >> 3)] = v;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(pr.empty + slot);
-      if (mt.last) {
-        ++k;
-        break;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(hempty);
-  }
-  team_sync(team);
-  if (tt == 0) res_sched_done(g, SCHED_INTERP, nteams);
-}
-
 
 // ------------------------------------------------ nodes with 2m+1 wide stencils
 // One warp per such node (rare: n x an exact integer in some dim): window
 // factors evaluated directly (kernels.py:42-53), the stencil walked by the
-// lanes; spread with atomics into the dense grid, interp with a warp sum.
-template <typename R, bool SPREAD>
+// lanes, atomics into the dense grid.
+template <typename R>
 __global__ void __launch_bounds__(256)
-k_wide_nodes(cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ f, const unsigned* __restrict__ rrec,
-             const double* __restrict__ xs, const int* __restrict__ perm, Geom g) {
-  // SPREAD: grid is the dense n-grid; interp: the ghost-padded copy (slot s at s + m)
+k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, const unsigned* __restrict__ rrec,
+             const double* __restrict__ xs, Geom g) {
   using C = cplx_t<R>;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -589,7 +286,6 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ f, const unsi
     while (todo) {
       const int64_t j = base + __ffs(todo) - 1;
       todo &= todo - 1;
-      // lanes 0 .. 3K-1 evaluate the (dim, offset) factors once
       int64_t lo[3];
       int wd[3];
 #pragma unroll
@@ -598,14 +294,13 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ f, const unsi
         lo[dim] = st.lo;
         wd[dim] = st.width;
       }
+      // lanes 0 .. 3K-1 evaluate the (dim, offset) factors once
       double fac = 0.0;
       if (lane < 3 * K) {
         const int dim = lane / K, t = lane - dim * K;
         if (t < wd[dim]) fac = dim_factor(g, dim, xs[dim * g.M + j], lo[dim] + t) * g.wscale[dim];
       }
-      C fj = C{0, 0};
-      if (SPREAD) fj = f[j];
-      double sr = 0, si = 0;
+      const C fj = fs[j];
       const int cells = wd[0] * wd[1] * wd[2];
       for (int q0 = 0; q0 < cells; q0 += 32) {
         const int q = q0 + lane;
@@ -616,31 +311,10 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, cplx_t<R>* __restrict__ f, const unsi
                      f2 = __shfl_sync(~0u, fac, 2 * K + t2);
         if (!on) continue;
         const double wgt = f0 * f1 * f2;
-        const int64_t s0 = floor_mod(lo[0] + t0, g.n[0]), s1 = floor_mod(lo[1] + t1, g.n[1]),
-                      s2 = floor_mod(lo[2] + t2, g.n[2]);
-        const int64_t idx = SPREAD ? (s0 * g.n[1] + s1) * g.n[2] + s2
-                                   : ((s0 + g.m) * g.np[1] + s1 + g.m) * g.np[2] + s2 + g.m;
-        if (SPREAD) {
-          atomicAdd(&grid[idx].x, (R)(fj.x * wgt));
-          atomicAdd(&grid[idx].y, (R)(fj.y * wgt));
-        } else {
-          const C v = grid[idx];
-          sr += (double)v.x * wgt;
-          si += (double)v.y * wgt;
-        }
-      }
-      if (!SPREAD) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          sr += __shfl_xor_sync(~0u, sr, o);
-          si += __shfl_xor_sync(~0u, si, o);
-        }
-        if (lane == 0) {
-          C v;
-          v.x = (R)sr;
-          v.y = (R)si;
-          f[perm[j]] = v;
-        }
+        const int64_t idx = (floor_mod(lo[0] + t0, g.n[0]) * g.n[1] + floor_mod(lo[1] + t1, g.n[1])) * g.n[2] +
+                            floor_mod(lo[2] + t2, g.n[2]);
+        atomicAdd(&grid[idx].x, (R)(fj.x * wgt));
+        atomicAdd(&grid[idx].y, (R)(fj.y * wgt));
       }
     }
   }
@@ -657,7 +331,7 @@ bool res_geometry(const Geom& g, bool single) {
 }
 
 bool res_ok(const Geom& g) {
-  return g.res && g.mode == MODE_TENSOR && g.psi && g.rrec && g.psi_pad == 3 && g.dense_flush;
+  return g.res && g.mode == MODE_TENSOR && g.psi && g.rrec && g.psi_pad == 2 && g.dense_flush;
 }
 
 static int sm_count() {
@@ -670,72 +344,37 @@ static int sm_count() {
   return sms;
 }
 
-static Geom res_sched_geom(const Geom& g, int nsubs, int nteams) {
-  Geom q = g;
-  if ((int64_t)nsubs < 4LL * nteams) q.sched = nullptr;
-  return q;
-}
-
-template <int NT, int NB, int S>
+template <int NB, int S, int BLOCKS>
 static void spread_res_go(void* grid, const void* fs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  using P = ResCfg<double, NT, NB, S, false>;
-  static_assert(P::SMEM <= 227 * 1024, "residue spread: shared memory");
-  auto kern = k_spread_res<double, NT, NB, S>;
+  using P = AresCfg<double, NB, S>;
+  static_assert(BLOCKS * (P::SMEM + 1024) <= 228 * 1024, "residue spread: shared memory per SM");
+  auto kern = k_spread_res<double, NB, S, BLOCKS>;
   NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
-  const int grid_x = std::max(1, std::min((nsubs + NT - 1) / NT, sm_count()));
-  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((double2*)grid, (const double2*)fs, g.psi, g.rrec, subs, nsubs,
-                                          res_sched_geom(g, nsubs, grid_x * NT));
+  int per_sm = 0;
+  NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
+  const int grid_x = std::max(1, std::min(nsubs, sm_count() * std::max(1, per_sm)));
+  Geom q = g;
+  if ((int64_t)nsubs < 4LL * grid_x) q.sched = nullptr;  // static order (gridding.cu sched_geom)
+  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((double2*)grid, (const double2*)fs, g.psi, g.rrec, subs, nsubs, q);
   count_launch();
-}
-
-template <int NT, int NB, int S>
-static void interp_res_go(const CUtensorMap* tm, void* f, const int* perm, const int4* subs, int nsubs,
-                          const Geom& g, cudaStream_t s) {
-  using P = ResCfg<double, NT, NB, S, true>;
-  static_assert(P::SMEM <= 227 * 1024, "residue interp: shared memory");
-  auto kern = k_interp_res<double, NT, NB, S>;
-  NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
-  const int grid_x = std::max(1, std::min((nsubs + NT - 1) / NT, sm_count()));
-  kern<<<grid_x, P::THREADS, P::SMEM, s>>>(*tm, (double2*)f, g.psi, g.rrec, perm, subs, nsubs,
-                                          res_sched_geom(g, nsubs, grid_x * NT));
-  count_launch();
-}
-
-static int res_teams() {
-  static int nt = 0;
-  if (!nt) {
-    const char* e = getenv("NFFTK_RES_TEAMS");
-    nt = e ? atoi(e) : 4;
-    if (nt != 3 && nt != 4) nt = 4;
-  }
-  return nt;
 }
 
 // B^H into the dense grid (zeroed by the caller): regular nodes by the
 // residue kernel, wide ones (g.nwide of them) by k_wide_nodes.
 void launch_spread_res(void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
                        const Geom& g, cudaStream_t s) {
-  if (res_teams() == 3) spread_res_go<3, 16, 6>(grid, fs, subs, nsubs, g, s);
-  else spread_res_go<4, 4, 4>(grid, fs, subs, nsubs, g, s);
-  if (g.nwide > 0) {
-    Geom q = g;
-    q.mode = MODE_DIRECT;
-    k_wide_nodes<double, true><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (double2*)fs, g.rrec, xs, nullptr, q);
-    count_launch();
+  // ring shape / CTAs per SM (A/B knob; the default is the measured best)
+  const char* e = getenv("NFFTK_RES_VARIANT");
+  switch (e ? atoi(e) : 0) {
+    case 1: spread_res_go<16, 4, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 2: spread_res_go<32, 2, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 3: spread_res_go<32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
+    default: spread_res_go<16, 3, 5>(grid, fs, subs, nsubs, g, s); break;
   }
-}
-
-// B from the ghost-padded grid gp (tensor map tm: 15^3 boxes); f is zeroed first (the two
-// warps of a team add their halves of a sample).
-void launch_interp_res(const void* tm, const void* gp, void* f, const double* xs, const int* perm,
-                       const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  NFFTK_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * (size_t)g.M, s));
-  if (res_teams() == 3) interp_res_go<3, 16, 6>((const CUtensorMap*)tm, f, perm, subs, nsubs, g, s);
-  else interp_res_go<4, 4, 4>((const CUtensorMap*)tm, f, perm, subs, nsubs, g, s);
   if (g.nwide > 0) {
     Geom q = g;
     q.mode = MODE_DIRECT;
-    k_wide_nodes<double, false><<<sm_count() * 4, 256, 0, s>>>((double2*)gp, (double2*)f, g.rrec, xs, perm, q);
+    k_wide_nodes<double><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (const double2*)fs, g.rrec, xs, q);
     count_launch();
   }
 }

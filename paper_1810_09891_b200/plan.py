@@ -357,9 +357,9 @@ class Plan:
 
     @property
     def gridding(self):
-        """Extension: which B / B^H kernels a PRE_PSI plan runs -- "residue"
-        (residue.cu: d=3, m=4, 8^3 tiles), "pipe" (row-per-thread pipelined
-        kernels) or "batch"."""
+        """Extension: which gridding kernels a PRE_PSI plan runs -- "residue"
+        (residue.cu spread + pipelined interp: d=3, m=4, 8^3 tiles), "pipe"
+        (row-per-thread pipelined kernels) or "batch"."""
         return ("batch", "pipe", "residue")[int(self._params()[13])]
 
     @property
