@@ -50,7 +50,7 @@ struct AresCfg {
   static constexpr int PR = psi_row_pad<R>(sten3_count(K));  // sten3 PRE_PSI row (common.cuh)
   static constexpr int OW0 = sten3_ow0(K), OW1 = sten3_ow1(K);
   static constexpr int THREADS = 128;                     // 16 x 8 lanes, b = 15 idle
-  static constexpr int ROWS = RES_H * 8;
+  static constexpr int ROWS = THREADS;                    // one staging row per lane
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
   static constexpr size_t ROWS_BYTES = al((size_t)ROWS * RES_H * ELEM);
   static constexpr size_t W_BYTES = al(sizeof(R) * NB * PR);
@@ -59,7 +59,7 @@ struct AresCfg {
   static constexpr size_t SB = W_BYTES + R_BYTES + F_BYTES;
   static constexpr size_t RING_OFF = ROWS_BYTES;
   static constexpr size_t CTL_OFF = RING_OFF + S * SB;
-  static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 32);
+  static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 48);
 };
 
 #define NFFTK_ARES_NODE(H)                                                                 \
@@ -122,16 +122,22 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
   using P = AresCfg<R, NB, S>;
   constexpr int K = P::K, PR = P::PR;
   static_assert(NB <= 32, "one ballot per batch");
+#ifdef NFFTK_RES_NO_ALT
+  constexpr int ALT = 0;
+#else
+  constexpr int ALT = 2;
+#endif
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL_OFF);
   unsigned long long* empty = full + S;
   AresMeta* meta = reinterpret_cast<AresMeta*>(empty + S);
   int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = threadIdx.x >> 3, ra = threadIdx.x & 7;
-  const bool owner = b < RES_H;
-  const int wb_lo = warp * 4, wb_hi = warp * 4 + 3;
-  C* const myrow = reinterpret_cast<C*>(smem) + (size_t)(owner ? threadIdx.x : 0) * RES_H;
+  const int ra = threadIdx.x & 7;
+  C* const myrow = reinterpret_cast<C*>(smem) + (size_t)threadIdx.x * RES_H;  // this lane's staging row
+  // pst[5] is the subproblem after pst[0], drawn one ahead so that its node
+  // data (PRE_PSI rows, records, samples) is pulled into L2 while the current
+  // one is spread: the ring's bulk copies then see L2 latency, not HBM's
   auto load_sub = [&](int s) {
     pst[0] = s;
     if (s < nsubs) {
@@ -139,6 +145,14 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       pst[1] = sp.y;
       pst[2] = sp.y + sp.z;
       pst[3] = sp.x;
+      const int nx = next_sub(g, SCHED_SPREAD3, s);
+      pst[5] = nx;
+      if (nx < nsubs) {
+        const int4 sn = subs[nx];
+        l2_prefetch(psi + (int64_t)sn.y * PR, (unsigned)(sizeof(R) * PR) * (unsigned)sn.z);
+        l2_prefetch(fsorted + (sn.y & ~1), (unsigned)sizeof(C) * (unsigned)((sn.z + 2) & ~1));
+        l2_prefetch(rrec + (sn.y & ~3), 4u * (unsigned)((sn.z + 6) & ~3));
+      }
     }
   };
   auto produce = [&]() {
@@ -170,7 +184,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     bulk_g2s(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
     if (pbase + nb < pend) pst[1] = pbase + nb;
-    else load_sub(next_sub(g, SCHED_SPREAD3, pst[0]));
+    else load_sub(pst[5]);
   };
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -189,7 +203,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
   for (int c = 0; c < RES_H; ++c) accr[c] = acci[c] = 0;
   // stage this lane's registers in its shared row and reduce them into the
   // dense grid row (a, b) of the tile (halo cell = slot tile * 8 - (m - 1) + cell)
-  auto flush_row = [&](int tile, int a) {
+  auto flush_row = [&](int tile, int a, int b) {
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // the row's previous reduction has read it
 #pragma unroll
     for (int c = 0; c < RES_H; ++c) {
@@ -210,7 +224,15 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     asm volatile("cp.async.bulk.commit_group;\n" ::);
   };
   int k = 0;
-  for (;;) {  // subproblems of this CTA
+  for (int par = 0;; par ^= ALT) {  // subproblems of this CTA
+    // A warp holds four b values.  The nodes' dim-1 windows [h_1, h_1 + 7]
+    // meet the four groups 50 / 100 / 87.5 / 37.5 % of the time and warp w of
+    // every CTA runs on SM sub-partition w, so a warp takes group w on even
+    // subproblems and group w + 2 on odd ones: 68.75 % each over a pair.
+    const int bgroup = (warp + par) & 3;
+    const int b = bgroup * 4 + (lane >> 3);
+    const bool owner = b < RES_H;
+    const int wb_lo = bgroup * 4, wb_hi = bgroup * 4 + 3;
     int tile = -1;
     bool upper = false;    // this lane holds row ra + 8 (the nodes' dim-0 start has passed ra)
     bool touched = false;  // a node met this warp's rows since its registers were zeroed
@@ -242,7 +264,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
         const int a0 = (int)(key & 7);
         // nodes come by ascending h_0: once it passes ra, row ra is complete
         if (owner && !upper && ra < a0) {
-          if (touched) flush_row(tile, ra);
+          if (touched) flush_row(tile, ra, b);
           upper = true;
         }
         touched = true;
@@ -261,7 +283,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       }
     }
     if (tile < 0) break;  // end of work
-    if (owner && touched) flush_row(tile, ra + (upper ? 8 : 0));
+    if (owner && touched) flush_row(tile, ra + (upper ? 8 : 0), b);
   }
   if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD3);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -363,13 +385,16 @@ static void spread_res_go(void* grid, const void* fs, const int4* subs, int nsub
 // residue kernel, wide ones (g.nwide of them) by k_wide_nodes.
 void launch_spread_res(void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
                        const Geom& g, cudaStream_t s) {
-  // ring shape / CTAs per SM (A/B knob; the default is the measured best)
+  // ring shape / CTAs per SM: batches of 32 on a 3-deep ring, 3 CTAs per SM
+  // measured best at C5 (20.4 ms; <16,3,5> 23.2, <16,4,4> 22.2, <32,2,4> 21.4,
+  // <32,4,3> 23.4); NFFTK_RES_VARIANT keeps the others for A/B runs
   const char* e = getenv("NFFTK_RES_VARIANT");
   switch (e ? atoi(e) : 0) {
-    case 1: spread_res_go<16, 4, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 2: spread_res_go<32, 2, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 3: spread_res_go<32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
-    default: spread_res_go<16, 3, 5>(grid, fs, subs, nsubs, g, s); break;
+    case 1: spread_res_go<16, 3, 5>(grid, fs, subs, nsubs, g, s); break;
+    case 2: spread_res_go<16, 4, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 3: spread_res_go<32, 2, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 4: spread_res_go<32, 4, 3>(grid, fs, subs, nsubs, g, s); break;
+    default: spread_res_go<32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
   }
   if (g.nwide > 0) {
     Geom q = g;

@@ -79,7 +79,7 @@ def test_residue_anisotropic(oracle, monkeypatch):
     check(plan(N, n, x, monkeypatch), N, n, x, oracle)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("kind", ["uniform", "clustered", "dense"])
 def test_residue_node_sets(kind, variant, oracle, monkeypatch):
     N, n = (16, 16, 16), (32, 32, 32)
