@@ -362,7 +362,8 @@ def main():
     peaks = measured_peaks()
     fp64, fp32 = ctypes_fma_peaks(_lib)
     roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32,
-                    tuple(plan.tile), args.psi, sm_mhz=clk.get("sm_mhz") or clk.get("sm_max_mhz"))
+                    tuple(plan.tile), args.psi, sm_mhz=clk.get("sm_mhz") or clk.get("sm_max_mhz"),
+                    gridding=plan.gridding)
 
     if rank != 0:
         if world > 1:
@@ -504,12 +505,14 @@ def ncu_traffic(config, kernel):
     return best
 
 
-def kernel_names(w, tile, psi):
+def kernel_names(w, tile, psi, gridding=None):
     """Names of the interp / spread kernels the library launches for this
     workload (gridding.cu launchers): the pipelined register kernels in
     PRE_PSI mode on their tile geometries, the batch kernels otherwise."""
     tensor = psi in (None, "flags", "tensor")
     k = 2 * w.m + 1
+    if gridding == "residue":  # residue.cu: d=3, m=4, 8^3 tiles, complex128
+        return {"interp": "k_interp_pipe", "spread": "k_spread_res"}
     if tensor and w.d == 3 and w.m <= 6 and tuple(tile) == (8, 8, 8):
         return {"interp": "k_interp_pipe", "spread": "k_spread_pipe"}
     if tensor and w.d == 2 and w.m <= 8 and tuple(tile) == (32 - k, 8):
@@ -523,7 +526,8 @@ def kernel_names(w, tile, psi):
 # roofline, reported with the compulsory bytes.
 BINDING = {
     "interp": "shared-memory wavefronts (one 16-byte halo cell per node-cell)",
-    "spread": "FP64 FMA issue and per-node latency of the register-resident halo walk",
+    "spread": "instruction issue of the register-resident halo walk (FP64 FMAs plus the per-node "
+              "factor loads and control)",
 }
 
 
@@ -545,12 +549,12 @@ def smem_roof(w, s, per_ms, sm_mhz):
             "peak_source": f"{sms} SMs x 128 B/clk x {sm_mhz:.0f} MHz (sampled SM clock)"}
 
 
-def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None, sm_mhz=None):
+def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None, sm_mhz=None, gridding=None):
     """Dominant gridding kernel vs measured HBM (SURVEY 8(d) compulsory bytes:
     M (8d + s) + s |I_n| + 4 M for the permutation) and vs the FMA roof
     (4 w^d M flops with w = 2m).  Times are CUDA-event durations of the kernel
     launches inside the timed region (library phase events on the launch stream)."""
-    kernels = kernel_names(w, tile, psi)
+    kernels = kernel_names(w, tile, psi, gridding)
     out = {}
     for ph, kname in kernels.items():
         ms, calls = phases.get(ph, (0.0, 0))
