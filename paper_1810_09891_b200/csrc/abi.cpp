@@ -227,7 +227,20 @@ static int32_t set_complex(int32_t h, const double* values, int64_t len, bool fh
       fail(EK_SHAPE, std::string(fhat ? "fhat" : "f") + " needs " + std::to_string(2 * count) +
                          " interleaved doubles, got " + std::to_string(len));
     double* dst = fhat ? fhat_buf(p) : f_buf(p);
-    par_memcpy(dst, values, sizeof(double) * 2 * count);
+    const size_t bytes = sizeof(double) * 2 * (size_t)count;
+    if (!plan_host_upload_begin(p, fhat)) {
+      par_memcpy(dst, values, bytes);
+      return;
+    }
+    // chunks: each is copied into the pinned library buffer, then queued for
+    // the device -- the PCIe transfer of chunk i runs under the copy of chunk i + 1
+    const size_t chunk = (size_t)32 << 20;
+    for (size_t off = 0; off < bytes; off += chunk) {
+      const size_t nb = std::min(chunk, bytes - off);
+      par_memcpy((char*)dst + off, (const char*)values + off, nb);
+      plan_host_upload_chunk(p, fhat, off, nb);
+    }
+    plan_host_upload_end(p, fhat);
   });
 }
 

@@ -107,6 +107,22 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
       : "memory");
 }
 
+// The same copy for streamed-once data (node batches): L2 evict-first, so the
+// stream does not push the grid lines the tiles share out of L2.
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void* sdst, const void* gsrc, unsigned bytes,
+                                                unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // TMA bulk reduction shared -> global (L2 performs the adds)
 template <typename R>
 __device__ __forceinline__ void bulk_red_add(void* gdst, const void* ssrc, unsigned bytes) {

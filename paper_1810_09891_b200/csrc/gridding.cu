@@ -657,9 +657,17 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
     unsigned char* st = smem + slot * P::SB;
     const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb, pb = 4u * pcnt;
     mbar_expect_tx(full + slot, wb + rb + pb);
+#ifdef NFFTK_NO_STREAM_HINT
     bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, perm + (pbase - poff), pb, full + slot);
+#else
+    // streamed once: L2 evict-first keeps the halo boxes the tiles share resident
+    const unsigned long long pol = l2_evict_first_policy();
+    bulk_g2s_stream(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot, pol);
+    bulk_g2s_stream(st + P::W_BYTES, rec + pbase, rb, full + slot, pol);
+    bulk_g2s_stream(st + P::W_BYTES + P::R_BYTES, perm + (pbase - poff), pb, full + slot, pol);
+#endif
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {

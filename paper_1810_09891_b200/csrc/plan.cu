@@ -755,8 +755,33 @@ static bool is_pinned(const void* h) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// nfftk_set_fhat / nfftk_set_f (cabi.py:149-160 copy into the library buffer):
+// the copy into the pinned library buffer goes chunk by chunk, each chunk
+// followed by its host-to-device copy on the plan's stream, so the PCIe
+// transfer runs under the host copy and the transform that follows finds its
+// input on the device.  complex128 plans with pinned buffers only.
+bool plan_host_upload_begin(Plan* p, bool fhat) {
+  (fhat ? p->fhat_dev_cur : p->f_dev_cur) = false;
+  if (p->single || p->d > MAX_D || getenv("NFFTK_NO_EAGER_UPLOAD")) return false;
+  if (!(fhat ? p->fhat_pinned : p->f_pinned)) return false;
+  NFFTK_CUDA(cudaSetDevice(p->device));
+  ensure_stream(p);
+  ensure_io(p);
+  NFFTK_CUDA(cudaStreamSynchronize(p->own_stream));  // an earlier upload still reads the buffer
+  return true;
+}
+
+void plan_host_upload_chunk(Plan* p, bool fhat, size_t off, size_t bytes) {
+  char* dev = (char*)(fhat ? p->fhat_dev : p->f_dev);
+  const char* host = (const char*)(fhat ? p->fhat_host : p->f_host);
+  NFFTK_CUDA(cudaMemcpyAsync(dev + off, host + off, bytes, cudaMemcpyHostToDevice, p->own_stream));
+}
+
+void plan_host_upload_end(Plan* p, bool fhat) { (fhat ? p->fhat_dev_cur : p->f_dev_cur) = true; }
+
 static void trafo_host_body(Plan* p, const void* fhat, void* f, cudaStream_t s) {
-  { PhaseScope ps(p, PH_H2D, s);
+  if (!(fhat == p->fhat_host && p->fhat_dev_cur)) {
+    PhaseScope ps(p, PH_H2D, s);
     NFFTK_CUDA(cudaMemcpyAsync(p->fhat_dev, fhat, p->elem_bytes() * p->num_freqs,
                                cudaMemcpyHostToDevice, s)); }
   plan_trafo_device(p, p->fhat_dev, p->f_dev, s);
@@ -765,7 +790,8 @@ static void trafo_host_body(Plan* p, const void* fhat, void* f, cudaStream_t s) 
 }
 
 static void adjoint_host_body(Plan* p, const void* f, void* fhat, cudaStream_t s) {
-  { PhaseScope ps(p, PH_H2D, s);
+  if (!(f == p->f_host && p->f_dev_cur)) {
+    PhaseScope ps(p, PH_H2D, s);
     NFFTK_CUDA(cudaMemcpyAsync(p->f_dev, f, p->elem_bytes() * p->M, cudaMemcpyHostToDevice, s)); }
   plan_adjoint_device(p, p->f_dev, p->fhat_dev, s);
   { PhaseScope ps(p, PH_D2H, s);
@@ -782,13 +808,18 @@ template <typename Body>
 static void host_call(Plan* p, int dir, const void* in, void* out, Body body) {
   cudaStream_t s = p->own_stream;
   Plan::HostGraph& h = p->hgraph[dir];
-  const bool same = h.in == in && h.out == out && h.gen == p->gen;
+  // whether this call's input is already on the device (set_fhat / set_f
+  // uploaded it, or it is the previous transform's result): part of the key,
+  // a captured graph either contains the host-to-device copy or does not
+  const bool skip = dir == 0 ? (in == p->fhat_host && p->fhat_dev_cur) : (in == p->f_host && p->f_dev_cur);
+  const bool same = h.in == in && h.out == out && h.gen == p->gen && h.skip_h2d == skip;
   if (!same) {
     if (h.exec) cudaGraphExecDestroy(h.exec);
     h = Plan::HostGraph();
     h.in = in;
     h.out = out;
     h.gen = p->gen;
+    h.skip_h2d = skip;
   }
   const bool usable = !p->graphs_off && !p->timing && !getenv("NFFTK_NO_HOST_GRAPH") &&
                       is_pinned(in) && is_pinned(out);
@@ -835,6 +866,9 @@ void plan_trafo_host(Plan* p, const void* fhat, void* f) {
   ensure_stream(p);
   ensure_io(p);
   host_call(p, 0, fhat, f, [&](cudaStream_t s) { trafo_host_body(p, fhat, f, s); });
+  // f_dev holds the samples just copied to f; fhat_dev still holds the input
+  p->f_dev_cur = f == p->f_host;
+  p->fhat_dev_cur = fhat == p->fhat_host;
 }
 
 void plan_adjoint_host(Plan* p, const void* f, void* fhat) {
@@ -843,6 +877,8 @@ void plan_adjoint_host(Plan* p, const void* f, void* fhat) {
   ensure_io(p);
   if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * (p->M + 2)));
   host_call(p, 1, f, fhat, [&](cudaStream_t s) { adjoint_host_body(p, f, fhat, s); });
+  p->fhat_dev_cur = fhat == p->fhat_host;
+  p->f_dev_cur = f == p->f_host;
 }
 
 void plan_node_order(Plan* p, int64_t* out) {

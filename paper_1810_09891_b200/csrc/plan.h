@@ -69,6 +69,10 @@ struct Plan {
   bool tmap_ready = false;
   void* fhat_dev = nullptr;
   void* f_dev = nullptr;
+  // the device copy equals the library-owned host buffer (uploaded by
+  // nfftk_set_fhat / nfftk_set_f, or the result of the last host transform):
+  // the next host transform skips its host-to-device copy
+  bool fhat_dev_cur = false, f_dev_cur = false;
   void* f_sorted = nullptr;         // spread input in tile-sorted order
   cufftHandle fft = 0;
   bool fft_ready = false;
@@ -88,6 +92,7 @@ struct Plan {
     const void* in = nullptr;
     void* out = nullptr;
     uint64_t gen = ~0ull;
+    bool skip_h2d = false;
     int seen = 0;
     unsigned long long launches = 0;
   };
@@ -118,6 +123,10 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s);
 void plan_interp_device(Plan* p, void* f, cudaStream_t s);
 std::vector<double> plan_deconv_cols(const Plan* p, int dim);
 void plan_adjoint_finish_device(Plan* p, void* fhat, cudaStream_t s);
+// nfftk_set_fhat / nfftk_set_f upload the library buffer while it is being filled
+bool plan_host_upload_begin(Plan* p, bool fhat);
+void plan_host_upload_chunk(Plan* p, bool fhat, size_t off, size_t bytes);
+void plan_host_upload_end(Plan* p, bool fhat);
 void plan_trafo_host(Plan* p, const void* fhat, void* f);
 void plan_adjoint_host(Plan* p, const void* f, void* fhat);
 // exact sums (ndft.cu), complex128 in and out

@@ -180,9 +180,16 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     const unsigned wb = (unsigned)(sizeof(R) * PR) * nb, rb = 4u * rcnt,
                    fb = (unsigned)P::ELEM * ((nb + foff + FA - 1) & ~(FA - 1));
     mbar_expect_tx(full + slot, wb + rb + fb);
+#ifdef NFFTK_NO_STREAM_HINT
     bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot);
     bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+#else
+    const unsigned long long pol = l2_evict_first_policy();
+    bulk_g2s_stream(st, psi + (int64_t)pbase * PR, wb, full + slot, pol);
+    bulk_g2s_stream(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot, pol);
+    bulk_g2s_stream(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot, pol);
+#endif
     if (pbase + nb < pend) pst[1] = pbase + nb;
     else load_sub(pst[5]);
   };

@@ -293,6 +293,54 @@ def test_abi_matches_python_api_bitwise():
     assert lib.nfftk_destroy(h) == 0
 
 
+def test_abi_uploaded_buffers_and_chained_transforms(oracle):
+    """nfftk_set_fhat / nfftk_set_f upload the library buffer while filling it
+    and the following transform skips its host-to-device copy; a transform's
+    result also stays on the device as the next one's input.  Every order of
+    set / transform calls must see the latest buffer contents: repeated sets,
+    transforms without a set in between (adjoint of the trafo result, trafo
+    of the adjoint result), and replays of each captured graph."""
+    N, n, m, M = (32, 32, 32), (64, 64, 64), 4, 150000
+    rng = np.random.default_rng(21)
+    x = rng.random((M, 3)) - 0.5
+    K = int(np.prod(N))
+    lib = _lib.load()
+    h = lib.nfftk_create_advanced(_lib.i32_array(N), 3, M, _lib.i32_array(n), m, 0x1fd1, 0x41)
+    assert h > 0
+    assert lib.nfftk_set_x(h, x.ctypes.data, x.size) == 0, lib.nfftk_last_error_message(h)
+
+    def cplx(k):
+        return rng.standard_normal(k) + 1j * rng.standard_normal(k)
+
+    def get(fn, k):
+        return np.ctypeslib.as_array(ctypes.cast(fn(h), ctypes.POINTER(ctypes.c_double)),
+                                     (2 * k,)).view(np.complex128).copy()
+
+    for rep in range(3):
+        fh_old, fh = cplx(K), cplx(K)
+        for v in (fh_old, fh):  # the second set wins
+            a = np.ascontiguousarray(v).view(np.float64)
+            assert lib.nfftk_set_fhat(h, a.ctypes.data, a.size) == 0
+        assert lib.nfftk_trafo(h) == 0
+        f1 = get(lib.nfftk_get_f, M)
+        assert e2(oracle.trafo(N, n, m, x, fh), f1) < TOL128
+        assert np.array_equal(get(lib.nfftk_get_fhat, K), fh)
+        # adjoint of the samples the trafo just produced (no set_f in between)
+        assert lib.nfftk_adjoint(h) == 0
+        a1 = get(lib.nfftk_get_fhat, K)
+        assert e2(oracle.adjoint(N, n, m, x, f1), a1) < TOL128
+        # trafo of the coefficients the adjoint just produced
+        assert lib.nfftk_trafo(h) == 0
+        assert e2(oracle.trafo(N, n, m, x, a1), get(lib.nfftk_get_f, M)) < TOL128
+        # a fresh set_f replaces the chained samples
+        fs = cplx(M)
+        b = np.ascontiguousarray(fs).view(np.float64)
+        assert lib.nfftk_set_f(h, b.ctypes.data, b.size) == 0
+        assert lib.nfftk_adjoint(h) == 0
+        assert e2(oracle.adjoint(N, n, m, x, fs), get(lib.nfftk_get_fhat, K)) < TOL128
+    assert lib.nfftk_destroy(h) == 0
+
+
 def test_abi_host_graph_replays_and_invalidation(oracle):
     """C-ABI calls on >= 1 MiB (pinned, library-owned) buffers run through a
     per-plan CUDA graph from the second call on: repeated calls reproduce the
