@@ -455,7 +455,8 @@ class DistributedPlan(DistributedNfft):
         if x.shape[0] != self.M_total:
             raise ValueError(f"set_nodes takes the global node set ({self.M_total} nodes), got {x.shape[0]}")
         self.shard_index = tile_shard_index(x, self.plan.n, self.plan.tile, self.world, self.rank)
-        self.plan.set_nodes(x.index_select(0, self.shard_index).contiguous())
+        # one rank owns every node in the given order: no gather of the coordinates
+        self.plan.set_nodes(x if self.world == 1 else x.index_select(0, self.shard_index).contiguous())
         self.engine.nodes_changed()
 
     def scatter(self, v):
