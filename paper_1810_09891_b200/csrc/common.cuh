@@ -134,12 +134,10 @@ struct Geom {
   const unsigned* rrec;   // res: 4-byte node records, sorted order (RES_* bits)
 };
 
-// Residue-owned spread (residue.cu): d = 3, m = 4, 8^3 tiles.  A regular node
-// (stencil 2m wide in every dim) touches halo cells h .. h + 7, h = its cell
-// inside the tile, of the 15^3 halo starting at slot tile * 8 - (m - 1).
-constexpr int RES_M = 4;
-constexpr int RES_W = 2 * RES_M;        // stencil width of a regular node
-constexpr int RES_H = 8 + RES_W - 1;    // halo edge
+// Residue-owned spread (residue.cu): d = 3, 8^3 tiles.  A regular node
+// (stencil 2m wide in every dim) touches halo cells h .. h + 2m - 1, h = its
+// cell inside the tile, of the (2m + 7)^3 halo starting at slot
+// tile * 8 - (m - 1).
 // record: h0 | h1 << 3 | h2 << 6 | regular << 9
 constexpr unsigned RES_REGULAR = 1u << 9;
 

@@ -2166,8 +2166,8 @@ void launch_interp(bool single, const void* tmap, const void* gp, void* f, const
 void launch_spread(bool single, void* gp, const void* f, void* fs, const double* xs,
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
-  if (!single && res_ok(g)) {  // gp: the dense grid (dense_flush)
-    launch_spread_res(gp, fs, xs, subs, nsubs, g, s);
+  if (res_ok(g)) {  // gp: the dense grid (dense_flush)
+    launch_spread_res(single, gp, fs, xs, subs, nsubs, g, s);
     return;
   }
   const CUtensorMap* tm = nullptr;

@@ -41,18 +41,36 @@ struct AresMeta {
   int off;   // offset of the records inside the stage (16-byte bulk copies)
 };
 
-template <typename R, int NB_, int S_>
+// Compile-time geometry for cutoff MM on 8^3 tiles: W = 2m residues of dim 0,
+// H = W + 7 halo cells per dim, H x W row lanes.
+template <typename R, int MM, int NB_, int S_>
 struct AresCfg {
   static constexpr int NB = NB_, S = S_;
-  static constexpr int K = 2 * RES_M + 1;
+  static constexpr int W = 2 * MM, H = W + 7, K = 2 * MM + 1;
   static constexpr int ELEM = 2 * (int)sizeof(R);
   static constexpr int FA = 16 / ELEM;                    // samples per 16 bytes
-  static constexpr int PR = psi_row_pad<R>(sten3_count(K));  // sten3 PRE_PSI row (common.cuh)
-  static constexpr int OW0 = sten3_ow0(K), OW1 = sten3_ow1(K);
-  static constexpr int THREADS = 128;                     // 16 x 8 lanes, b = 15 idle
-  static constexpr int ROWS = THREADS;                    // one staging row per lane
+  static constexpr int HO = 8 + K;                        // halo edge of the row-per-thread kernels (rows' index space)
+  // PRE_PSI row: sten3 blocks (c128, m <= 4) or halo-indexed [HO | HO | K] (common.cuh pipe_sten3)
+  static constexpr bool STEN3 = pipe_sten3(sizeof(R) == 4, MM);
+  static constexpr int PR = psi_row_pad<R>(STEN3 ? sten3_count(K) : 2 * HO + K);
+  static constexpr int OW0 = STEN3 ? sten3_ow0(K) : 0, OW1 = STEN3 ? sten3_ow1(K) : HO,
+                       OWL = STEN3 ? STEN3_OW2 : 2 * HO;
+  static constexpr int LANES = H * W;                     // row lanes: b = t / W, ra = t % W
+  static constexpr int THREADS = (LANES + 31) / 32 * 32;
+  static constexpr int NW = THREADS / 32;
+  // staging row: the H cells (complex64: one zero cell in front, so the row
+  // starts at an even slot and stays a multiple of 16 bytes -- m and n even),
+  // stride a multiple of 16 bytes with an odd number of 16-byte units: eight
+  // consecutive rows start in eight different bank groups
+  static constexpr int LEAD = ELEM == 8 ? 1 : 0;
+  static constexpr int ROW_CELLS = H + LEAD;
+  static constexpr int row_stride_bytes() {
+    int u = (ROW_CELLS * ELEM + 15) / 16;
+    return 16 * (u | 1);
+  }
+  static constexpr int RS = row_stride_bytes() / ELEM;    // row stride in cells
   static constexpr size_t al(size_t v) { return (v + 15) & ~(size_t)15; }
-  static constexpr size_t ROWS_BYTES = al((size_t)ROWS * RES_H * ELEM);
+  static constexpr size_t ROWS_BYTES = al((size_t)THREADS * RS * ELEM);
   static constexpr size_t W_BYTES = al(sizeof(R) * NB * PR);
   static constexpr size_t R_BYTES = al(4 * (size_t)(NB + 4));
   static constexpr size_t F_BYTES = al((size_t)ELEM * (NB + FA));
@@ -62,79 +80,79 @@ struct AresCfg {
   static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 48);
 };
 
-#define NFFTK_ARES_NODE(H)                                                                 \
-  {                                                                                        \
-    m2 &= m2 - 1;                                                                          \
-    const int jn = m2 ? __ffs(m2) - 1 : jj;                                                \
-    const unsigned rn = rs[jn]; /* next node's record, under this node's FMAs */           \
-    const R* pw = ws + jj * PR;                                                            \
-    const R s = pw[offa] * pw[P::OW1 + min((unsigned)(b - b0), (unsigned)K)];              \
-    const C f = fv[jj];                                                                    \
-    const R cr = f.x * s, ci = f.y * s;                                                    \
-    R w2[RES_W];                                                                           \
-    load8<R>(pw, w2);                                                                      \
-    _Pragma("unroll") for (int t = 0; t < RES_W; ++t) {                                    \
-      accr[H + t] = fma(cr, w2[t], accr[H + t]);                                           \
-      acci[H + t] = fma(ci, w2[t], acci[H + t]);                                           \
-    }                                                                                      \
-    jj = jn;                                                                               \
-    b0 = (int)((rn >> 3) & 7);                                                             \
-  }
-#define NFFTK_ARES_CASE(H)             \
-  case H: {                            \
-    unsigned m2 = run;                 \
-    int jj = __ffs(m2) - 1;            \
-    int b0 = (int)((rs[jj] >> 3) & 7); \
-    do {                               \
-      NFFTK_ARES_NODE(H)               \
-    } while (m2);                      \
-  } break;
-
-template <typename R>
-__device__ __forceinline__ void load8(const R* w, R* o) {
+// the W last-dim factors of a node (16-byte loads for fp64 rows, 8-byte for fp32 rows)
+template <typename R, int W>
+__device__ __forceinline__ void load_factors(const R* w, R* o) {
   if constexpr (sizeof(R) == 8) {
     const double2* p = reinterpret_cast<const double2*>(w);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < W / 2; ++i) {
       const double2 v = p[i];
       o[2 * i] = v.x;
       o[2 * i + 1] = v.y;
     }
   } else {
-    const float4* p = reinterpret_cast<const float4*>(w);
+    const float2* p = reinterpret_cast<const float2*>(w);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float4 v = p[i];
-      o[4 * i] = v.x;
-      o[4 * i + 1] = v.y;
-      o[4 * i + 2] = v.z;
-      o[4 * i + 3] = v.w;
+    for (int i = 0; i < W / 2; ++i) {
+      const float2 v = p[i];
+      o[2 * i] = v.x;
+      o[2 * i + 1] = v.y;
     }
   }
 }
 
-template <typename R, int NB, int S, int BLOCKS>
-__global__ void __launch_bounds__(128, BLOCKS)
+#define NFFTK_ARES_NODE(H2)                                                                \
+  {                                                                                        \
+    m2 &= m2 - 1;                                                                          \
+    const int jn = m2 ? __ffs(m2) - 1 : jj;                                                \
+    const unsigned rn = rs[jn]; /* next node's record, under this node's FMAs */           \
+    const R* pw = ws + jj * PR;                                                            \
+    R s;                                                                                   \
+    if constexpr (P::STEN3) s = pw[offa] * pw[P::OW1 + min((unsigned)(b - b0), (unsigned)K)]; \
+    else s = pw[offa] * pw[offb];                                                          \
+    const C f = fv[jj];                                                                    \
+    const R cr = f.x * s, ci = f.y * s;                                                    \
+    R w2[W];                                                                               \
+    load_factors<R, W>(pw + P::OWL, w2);                                                   \
+    _Pragma("unroll") for (int t = 0; t < W; ++t) {                                        \
+      accr[H2 + t] = fma(cr, w2[t], accr[H2 + t]);                                         \
+      acci[H2 + t] = fma(ci, w2[t], acci[H2 + t]);                                         \
+    }                                                                                      \
+    jj = jn;                                                                               \
+    b0 = (int)((rn >> 3) & 7);                                                             \
+  }
+#define NFFTK_ARES_CASE(H2)            \
+  case H2: {                           \
+    unsigned m2 = run;                 \
+    int jj = __ffs(m2) - 1;            \
+    int b0 = (int)((rs[jj] >> 3) & 7); \
+    do {                               \
+      NFFTK_ARES_NODE(H2)              \
+    } while (m2);                      \
+  } break;
+
+template <typename R, int MM, int NB, int S, int BLOCKS>
+__global__ void __launch_bounds__((AresCfg<R, MM, NB, S>::THREADS), BLOCKS)
 k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted,
              const R* __restrict__ psi, const unsigned* __restrict__ rrec,
              const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
-  using P = AresCfg<R, NB, S>;
-  constexpr int K = P::K, PR = P::PR;
+  using P = AresCfg<R, MM, NB, S>;
+  constexpr int K = P::K, PR = P::PR, W = P::W, H = P::H, NW = P::NW;
   static_assert(NB <= 32, "one ballot per batch");
 #ifdef NFFTK_RES_NO_ALT
   constexpr int ALT = 0;
 #else
-  constexpr int ALT = 2;
+  constexpr int ALT = NW / 2;
 #endif
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL_OFF);
   unsigned long long* empty = full + S;
   AresMeta* meta = reinterpret_cast<AresMeta*>(empty + S);
-  int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk, next sub
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ra = threadIdx.x & 7;
-  C* const myrow = reinterpret_cast<C*>(smem) + (size_t)threadIdx.x * RES_H;  // this lane's staging row
+  C* const myrow = reinterpret_cast<C*>(smem) + (size_t)threadIdx.x * P::RS;  // this lane's staging row
   // pst[5] is the subproblem after pst[0], drawn one ahead so that its node
   // data (PRE_PSI rows, records, samples) is pulled into L2 while the current
   // one is spread: the ring's bulk copies then see L2 latency, not HBM's
@@ -196,7 +214,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, P::THREADS / 32);
+      mbar_init(empty + i, NW);
     }
     pst[4] = 0;
     load_sub((int)blockIdx.x);
@@ -205,43 +223,45 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
   if (threadIdx.x == 0)
     for (int i = 0; i < S - 1; ++i) produce();
 
-  R accr[RES_H], acci[RES_H];
+  R accr[H], acci[H];
 #pragma unroll
-  for (int c = 0; c < RES_H; ++c) accr[c] = acci[c] = 0;
+  for (int c = 0; c < H; ++c) accr[c] = acci[c] = 0;
   // stage this lane's registers in its shared row and reduce them into the
   // dense grid row (a, b) of the tile (halo cell = slot tile * 8 - (m - 1) + cell)
   auto flush_row = [&](int tile, int a, int b) {
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // the row's previous reduction has read it
+    if constexpr (P::LEAD) myrow[0] = C{0, 0};
 #pragma unroll
-    for (int c = 0; c < RES_H; ++c) {
+    for (int c = 0; c < H; ++c) {
       C v;
       v.x = accr[c];
       v.y = acci[c];
-      myrow[c] = v;
+      myrow[P::LEAD + c] = v;
       accr[c] = acci[c] = 0;
     }
     fence_proxy_async_smem();
     int tc[3];
     tile_of<3>(g, tile, tc);
-    int ad = tc[0] * 8 - (RES_M - 1) + a, bd = tc[1] * 8 - (RES_M - 1) + b;
+    int ad = tc[0] * 8 - (MM - 1) + a, bd = tc[1] * 8 - (MM - 1) + b;
     ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
     bd += bd < 0 ? g.n[1] : (bd >= g.n[1] ? -g.n[1] : 0);
-    bulk_red_row_wrapped<R>(grid, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - (RES_M - 1), g.n[2], myrow,
-                            RES_H);
+    bulk_red_row_wrapped<R>(grid, ((int64_t)ad * g.n[1] + bd) * g.n[2], tc[2] * 8 - (MM - 1) - P::LEAD, g.n[2],
+                            myrow, P::ROW_CELLS);
     asm volatile("cp.async.bulk.commit_group;\n" ::);
   };
   int k = 0;
-  for (int par = 0;; par ^= ALT) {  // subproblems of this CTA
-    // A warp holds four b values.  The nodes' dim-1 windows [h_1, h_1 + 7]
-    // meet the four groups 50 / 100 / 87.5 / 37.5 % of the time and warp w of
-    // every CTA runs on SM sub-partition w, so a warp takes group w on even
-    // subproblems and group w + 2 on odd ones: 68.75 % each over a pair.
-    const int bgroup = (warp + par) & 3;
-    const int b = bgroup * 4 + (lane >> 3);
-    const bool owner = b < RES_H;
-    const int wb_lo = bgroup * 4, wb_hi = bgroup * 4 + 3;
+  for (int par = 0;; par = par ? 0 : ALT) {  // subproblems of this CTA
+    // A warp holds 32 / W consecutive b values.  The nodes' dim-1 windows
+    // [h_1, h_1 + W - 1] meet the b groups unevenly (m = 4: 50 / 100 / 87.5 /
+    // 37.5 % of the nodes) and warp w of every CTA runs on SM sub-partition
+    // w mod 4, so a warp takes group w on even subproblems and group
+    // w + NW / 2 on odd ones.
+    const int t = ((warp + par) % NW) * 32 + lane;
+    const int b = t / W, ra = t - b * W;
+    const bool owner = b < H;
+    const int wb_lo = (((warp + par) % NW) * 32) / W, wb_hi = min((((warp + par) % NW) * 32 + 31) / W, H - 1);
     int tile = -1;
-    bool upper = false;    // this lane holds row ra + 8 (the nodes' dim-0 start has passed ra)
+    int a = ra;            // this lane's row: the first a = ra (mod W) at or after the nodes' dim-0 start
     bool touched = false;  // a node met this warp's rows since its registers were zeroed
     for (;; ++k) {  // batches of the subproblem
       const int slot = k % S;
@@ -254,11 +274,11 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       const unsigned* rs = reinterpret_cast<const unsigned*>(st + P::W_BYTES) + mt.off;
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (P::FA > 1 ? (mt.off & (P::FA - 1)) : 0);
       // Per-batch warp view: lane l holds node l's record; one ballot gives
-      // the regular nodes whose dim-1 window meets this warp's four b values,
+      // the regular nodes whose dim-1 window meets this warp's b values,
       // another the starts of runs of equal (h_0, h_2).
       const unsigned rl = lane < mt.nb ? rs[lane] : 0u;
       const int bl = (int)((rl >> 3) & 7);
-      unsigned mask = __ballot_sync(~0u, (rl & RES_REGULAR) && bl <= wb_hi && bl + RES_W - 1 >= wb_lo);
+      unsigned mask = __ballot_sync(~0u, (rl & RES_REGULAR) && bl <= wb_hi && bl + W - 1 >= wb_lo);
       const unsigned kl = rl & 0x1c7u;
       const unsigned kup = __shfl_up_sync(~0u, kl, 1);
       const unsigned rstart = __ballot_sync(~0u, lane == 0 || kl != kup);
@@ -269,13 +289,24 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
         const unsigned run = later ? mask & ((later & (0u - later)) - 1u) : mask;
         mask &= ~run;
         const int a0 = (int)(key & 7);
-        // nodes come by ascending h_0: once it passes ra, row ra is complete
-        if (owner && !upper && ra < a0) {
-          if (touched) flush_row(tile, ra, b);
-          upper = true;
+        // nodes come by ascending h_0: once it passes a, row a is complete and
+        // the lane moves on to the next row of its residue (once per tile for
+        // W >= 8)
+        if (owner && a < a0) {
+          if (touched) flush_row(tile, a, b);
+          do a += W;
+          while (a < a0);
         }
         touched = true;
-        const int offa = P::OW0 + ((ra - a0) & 7);
+        // row a is stencil offset a - h_0 of the run's nodes; halo-indexed
+        // PRE_PSI rows hold the factor at the row's cell itself (index + 1:
+        // their halo starts one cell earlier)
+        const int offa = P::STEN3 ? P::OW0 + (a - a0) : P::OW0 + a + 1;
+        // (idle lanes, b >= H, read the block's last entry: zero for regular
+        // nodes, so their accumulators stay zero -- they may be row lanes of
+        // the next subproblem; sten3 rows clamp onto the block's zero instead)
+        const int offb = P::OW1 + min(b + 1, P::HO - 1);
+        (void)offb;
         switch (key >> 6) {
           NFFTK_ARES_CASE(0) NFFTK_ARES_CASE(1) NFFTK_ARES_CASE(2) NFFTK_ARES_CASE(3)
           NFFTK_ARES_CASE(4) NFFTK_ARES_CASE(5) NFFTK_ARES_CASE(6) NFFTK_ARES_CASE(7)
@@ -290,7 +321,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       }
     }
     if (tile < 0) break;  // end of work
-    if (owner && touched) flush_row(tile, ra + (upper ? 8 : 0), b);
+    if (owner && touched) flush_row(tile, a, b);
   }
   if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD3);
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -323,11 +354,12 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, con
         lo[dim] = st.lo;
         wd[dim] = st.width;
       }
-      // lanes 0 .. 3K-1 evaluate the (dim, offset) factors once
-      double fac = 0.0;
-      if (lane < 3 * K) {
-        const int dim = lane / K, t = lane - dim * K;
-        if (t < wd[dim]) fac = dim_factor(g, dim, xs[dim * g.M + j], lo[dim] + t) * g.wscale[dim];
+      // lane t < K evaluates the three factors of stencil offset t once
+      double fac[3] = {0.0, 0.0, 0.0};
+      if (lane < K) {
+#pragma unroll
+        for (int dim = 0; dim < 3; ++dim)
+          if (lane < wd[dim]) fac[dim] = dim_factor(g, dim, xs[dim * g.M + j], lo[dim] + lane) * g.wscale[dim];
       }
       const C fj = fs[j];
       const int cells = wd[0] * wd[1] * wd[2];
@@ -336,8 +368,8 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, con
         const bool on = q < cells;
         const int qq = on ? q : 0;
         const int t2 = qq % wd[2], t1 = (qq / wd[2]) % wd[1], t0 = qq / (wd[2] * wd[1]);
-        const double f0 = __shfl_sync(~0u, fac, t0), f1 = __shfl_sync(~0u, fac, K + t1),
-                     f2 = __shfl_sync(~0u, fac, 2 * K + t2);
+        const double f0 = __shfl_sync(~0u, fac[0], t0), f1 = __shfl_sync(~0u, fac[1], t1),
+                     f2 = __shfl_sync(~0u, fac[2], t2);
         if (!on) continue;
         const double wgt = f0 * f1 * f2;
         const int64_t idx = (floor_mod(lo[0] + t0, g.n[0]) * g.n[1] + floor_mod(lo[1] + t1, g.n[1])) * g.n[2] +
@@ -350,17 +382,25 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, con
 }
 
 // ================================================================ launchers
+// d = 3 plans on 8^3 tiles whose halo rows fit one period; complex64 needs m
+// and the last grid dim even (16-byte bulk reductions).  The kernel is
+// written for any m <= 6 (tests run m = 1..6 with NFFTK_RES_ANY_M), but only
+// m = 4 takes it by default: that is where it was measured against the
+// row-per-thread kernels and wins (C5: 33.5 -> 20.6 ms c128, 19.3 -> 12.6 ms
+// c64); at C3 (m = 6, 64 nodes per tile) it is level or behind (0.341 vs
+// 0.325 ms c128, 0.276 vs 0.246 ms c64).
 bool res_geometry(const Geom& g, bool single) {
   if (getenv("NFFTK_NO_RES") || getenv("NFFTK_NO_PIPE") || getenv("NFFTK_NO_DENSE_FLUSH")) return false;
-  if (single) return false;
-  if (g.d != 3 || g.m != RES_M) return false;
+  if (g.d != 3 || g.m < 1 || g.m > 6) return false;
+  if (g.m != 4 && !getenv("NFFTK_RES_ANY_M")) return false;
+  if (single && (g.m % 2 != 0 || g.n[2] % 2 != 0)) return false;
   for (int i = 0; i < 3; ++i)
-    if (g.T[i] != 8 || g.n[i] < 8 + 2 * RES_M + 1) return false;
+    if (g.T[i] != 8 || g.n[i] < 8 + 2 * g.m + 1) return false;
   return true;
 }
 
 bool res_ok(const Geom& g) {
-  return g.res && g.mode == MODE_TENSOR && g.psi && g.rrec && g.psi_pad == 2 && g.dense_flush;
+  return g.res && g.mode == MODE_TENSOR && g.psi && g.rrec && g.psi_pad != 0 && g.dense_flush;
 }
 
 static int sm_count() {
@@ -373,40 +413,62 @@ static int sm_count() {
   return sms;
 }
 
-template <int NB, int S, int BLOCKS>
+template <typename R, int MM, int NB, int S, int BLOCKS>
 static void spread_res_go(void* grid, const void* fs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
-  using P = AresCfg<double, NB, S>;
-  static_assert(BLOCKS * (P::SMEM + 1024) <= 228 * 1024, "residue spread: shared memory per SM");
-  auto kern = k_spread_res<double, NB, S, BLOCKS>;
+  using P = AresCfg<R, MM, NB, S>;
+  static_assert(P::SMEM <= 227 * 1024, "residue spread: shared memory");
+  if (g.psi_pad != (P::STEN3 ? 2 : 1) || (g.psi_f32 != 0) != (sizeof(R) == 4))
+    fail(EK_CUDA, "residue spread: PRE_PSI layout mismatch");
+  auto kern = k_spread_res<R, MM, NB, S, BLOCKS>;
   NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
   int per_sm = 0;
   NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
   const int grid_x = std::max(1, std::min(nsubs, sm_count() * std::max(1, per_sm)));
   Geom q = g;
   if ((int64_t)nsubs < 4LL * grid_x) q.sched = nullptr;  // static order (gridding.cu sched_geom)
-  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((double2*)grid, (const double2*)fs, g.psi, g.rrec, subs, nsubs, q);
+  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)grid, (const cplx_t<R>*)fs, (const R*)g.psi, g.rrec, subs,
+                                          nsubs, q);
   count_launch();
+}
+
+template <typename R>
+static void spread_res_m(void* grid, const void* fs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+  // ring shape / CTAs per SM.  m = 4, c128 (C5): batches of 32 on a 3-deep
+  // ring measured best (20.4 ms; <16,3,5> 23.2, <16,4,4> 22.2, <32,2,4> 21.4,
+  // <32,4,3> 23.4); NFFTK_RES_VARIANT keeps the others for A/B runs.  The
+  // wider rows of m >= 5 take batches of 16.
+  const char* e = getenv("NFFTK_RES_VARIANT");
+  const int v = e ? atoi(e) : 0;
+  switch (g.m) {
+    case 1: spread_res_go<R, 1, 32, 3, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 2: spread_res_go<R, 2, 32, 3, 4>(grid, fs, subs, nsubs, g, s); break;
+    case 3: spread_res_go<R, 3, 32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
+    case 4:
+      if (v == 1) spread_res_go<R, 4, 16, 3, 5>(grid, fs, subs, nsubs, g, s);
+      else if (v == 2) spread_res_go<R, 4, 16, 4, 4>(grid, fs, subs, nsubs, g, s);
+      else if (v == 3) spread_res_go<R, 4, 32, 2, 4>(grid, fs, subs, nsubs, g, s);
+      else if (v == 4) spread_res_go<R, 4, 32, 4, 3>(grid, fs, subs, nsubs, g, s);
+      else spread_res_go<R, 4, 32, 3, 3>(grid, fs, subs, nsubs, g, s);
+      break;
+    case 5: spread_res_go<R, 5, 16, 3, 2>(grid, fs, subs, nsubs, g, s); break;
+    default:
+      if (v == 1) spread_res_go<R, 6, 32, 2, 1>(grid, fs, subs, nsubs, g, s);
+      else spread_res_go<R, 6, 16, 3, 2>(grid, fs, subs, nsubs, g, s);
+      break;
+  }
 }
 
 // B^H into the dense grid (zeroed by the caller): regular nodes by the
 // residue kernel, wide ones (g.nwide of them) by k_wide_nodes.
-void launch_spread_res(void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
+void launch_spread_res(bool single, void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
                        const Geom& g, cudaStream_t s) {
-  // ring shape / CTAs per SM: batches of 32 on a 3-deep ring, 3 CTAs per SM
-  // measured best at C5 (20.4 ms; <16,3,5> 23.2, <16,4,4> 22.2, <32,2,4> 21.4,
-  // <32,4,3> 23.4); NFFTK_RES_VARIANT keeps the others for A/B runs
-  const char* e = getenv("NFFTK_RES_VARIANT");
-  switch (e ? atoi(e) : 0) {
-    case 1: spread_res_go<16, 3, 5>(grid, fs, subs, nsubs, g, s); break;
-    case 2: spread_res_go<16, 4, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 3: spread_res_go<32, 2, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 4: spread_res_go<32, 4, 3>(grid, fs, subs, nsubs, g, s); break;
-    default: spread_res_go<32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
-  }
+  if (single) spread_res_m<float>(grid, fs, subs, nsubs, g, s);
+  else spread_res_m<double>(grid, fs, subs, nsubs, g, s);
   if (g.nwide > 0) {
     Geom q = g;
     q.mode = MODE_DIRECT;
-    k_wide_nodes<double><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (const double2*)fs, g.rrec, xs, q);
+    if (single) k_wide_nodes<float><<<sm_count() * 4, 256, 0, s>>>((float2*)grid, (const float2*)fs, g.rrec, xs, q);
+    else k_wide_nodes<double><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (const double2*)fs, g.rrec, xs, q);
     count_launch();
   }
 }

@@ -1,6 +1,7 @@
 """Parity of the residue-owned d=3 spread (residue.cu: k_spread_res,
 k_wide_nodes; the interp of these plans is k_interp_pipe on the same node
-order) against the CPU oracle: m = 4 on 8^3 tiles, complex128.  Cases: grids
+order) against the CPU oracle: 8^3 tiles, every cutoff 1..6 in complex128 and
+the even ones in complex64; most cases at m = 4 (the C5 geometry).  Cases: grids
 whose tiles divide n and do not (partial last tiles), nodes on every periodic
 boundary, grid-aligned nodes (2m+1 wide stencils: the k_wide_nodes pass), one
 dense cell (several subproblems of one tile), clustered nodes, node counts
@@ -41,26 +42,57 @@ def nodes(n, M, seed, kind="uniform"):
     return x
 
 
-def plan(N, n, x, monkeypatch, variant=None):
+TOL = {"double": 1e-12, "single": 1e-5}
+
+
+def plan(N, n, x, monkeypatch, variant=None, m=M4, precision="double"):
     monkeypatch.setenv("NFFTK_TILE", "8")
+    monkeypatch.setenv("NFFTK_RES_ANY_M", "1")  # cutoffs other than 4 take the row kernels by default
     if variant is not None:
         monkeypatch.setenv("NFFTK_RES_VARIANT", str(variant))
-    p = nf.Plan(N, x.shape[0], n=n, m=M4)
+    else:
+        monkeypatch.delenv("NFFTK_RES_VARIANT", raising=False)
+    p = nf.Plan(N, x.shape[0], n=n, m=m, precision=precision)
     p.x = x
     p.precompute()
     assert p.tile == (8, 8, 8) and p.gridding == "residue"
     return p
 
 
-def check(p, N, n, x, oracle, reps=1):
+def check(p, N, n, x, oracle, reps=1, m=M4, precision="double"):
     rng = np.random.default_rng(7)
     fh = rng.standard_normal(int(np.prod(N))) + 1j * rng.standard_normal(int(np.prod(N)))
     fs = rng.standard_normal(x.shape[0]) + 1j * rng.standard_normal(x.shape[0])
-    rt = oracle.trafo(N, n, M4, x, fh)
-    ra = oracle.adjoint(N, n, M4, x, fs)
+    rt = oracle.trafo(N, n, m, x, fh)
+    ra = oracle.adjoint(N, n, m, x, fs)
     for _ in range(reps):
-        assert e2(rt, p.trafo(fh)) < 1e-12
-        assert e2(ra, p.adjoint(fs)) < 1e-12
+        assert e2(rt, p.trafo(fh)) < TOL[precision]
+        assert e2(ra, p.adjoint(fs)) < TOL[precision]
+
+
+@pytest.mark.parametrize("m,precision", [(1, "double"), (2, "double"), (3, "double"), (4, "double"), (5, "double"),
+                                         (6, "double"), (2, "single"), (4, "single"), (6, "single")])
+@pytest.mark.parametrize("n1,kind", [(32, "edges"), (28, "uniform"), (40, "clustered")])
+def test_residue_every_cutoff(m, precision, n1, kind, oracle, monkeypatch):
+    """Every instantiated cutoff and precision: nodes on the periodic
+    boundaries and grid-aligned (wide) nodes, a grid the tiles do not divide,
+    clustered nodes (tiles split into several subproblems)."""
+    N, n = (8, 8, 8), (n1, n1, n1)
+    x = nodes(n, 12000, seed=3 * m + n1, kind=kind)
+    p = plan(N, n, x, monkeypatch, m=m, precision=precision)
+    check(p, N, n, x, oracle, m=m, precision=precision, reps=2)
+
+
+def test_residue_odd_cutoff_single_uses_row_kernels(monkeypatch):
+    """complex64 bulk reductions need 16-byte pieces: odd m (odd row start)
+    stays on the row-per-thread kernels."""
+    monkeypatch.setenv("NFFTK_TILE", "8")
+    monkeypatch.setenv("NFFTK_RES_ANY_M", "1")
+    x = nodes((32, 32, 32), 5000, seed=1)
+    p = nf.Plan((8, 8, 8), 5000, n=(32, 32, 32), m=3, precision="single")
+    p.x = x
+    p.precompute()
+    assert p.gridding == "pipe"
 
 
 @pytest.mark.parametrize("n1", [24, 32, 20, 36, 18])
