@@ -102,16 +102,17 @@ __device__ __forceinline__ void load_factors(const R* w, R* o) {
   }
 }
 
+// One node of a run: the run's nodes are consecutive in the batch (a run is a
+// maximal range of consecutive nodes of equal (h_0, h_2) that hit this warp),
+// so the factor row, sample and record pointers advance by constants and the
+// next node's dim-1 start is read one node ahead.
 #define NFFTK_ARES_NODE(H2)                                                                \
   {                                                                                        \
-    m2 &= m2 - 1;                                                                          \
-    const int jn = m2 ? __ffs(m2) - 1 : jj;                                                \
-    const unsigned rn = rs[jn]; /* next node's record, under this node's FMAs */           \
-    const R* pw = ws + jj * PR;                                                            \
     R s;                                                                                   \
     if constexpr (P::STEN3) s = pw[offa] * pw[P::OW1 + min((unsigned)(b - b0), (unsigned)K)]; \
     else s = pw[offa] * pw[offb];                                                          \
-    const C f = fv[jj];                                                                    \
+    const unsigned rn = rp[1]; /* next node's record, under this node's FMAs */            \
+    const C f = *fp;                                                                       \
     const R cr = f.x * s, ci = f.y * s;                                                    \
     R w2[W];                                                                               \
     load_factors<R, W>(pw + P::OWL, w2);                                                   \
@@ -119,17 +120,21 @@ __device__ __forceinline__ void load_factors(const R* w, R* o) {
       accr[H2 + t] = fma(cr, w2[t], accr[H2 + t]);                                         \
       acci[H2 + t] = fma(ci, w2[t], acci[H2 + t]);                                         \
     }                                                                                      \
-    jj = jn;                                                                               \
+    pw += PR;                                                                              \
+    ++fp;                                                                                  \
+    ++rp;                                                                                  \
     b0 = (int)((rn >> 3) & 7);                                                             \
   }
-#define NFFTK_ARES_CASE(H2)            \
-  case H2: {                           \
-    unsigned m2 = run;                 \
-    int jj = __ffs(m2) - 1;            \
-    int b0 = (int)((rs[jj] >> 3) & 7); \
-    do {                               \
-      NFFTK_ARES_NODE(H2)              \
-    } while (m2);                      \
+#define NFFTK_ARES_CASE(H2)              \
+  case H2: {                             \
+    const R* pw = ws + j0 * PR;          \
+    const C* fp = fv + j0;               \
+    const unsigned* rp = rs + j0;        \
+    int b0 = (int)((rp[0] >> 3) & 7);    \
+    int cnt = __popc(run);               \
+    _Pragma("unroll 1") do {             \
+      NFFTK_ARES_NODE(H2)                \
+    } while (--cnt);                     \
   } break;
 
 template <typename R, int MM, int NB, int S, int BLOCKS>
@@ -278,8 +283,10 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       // another the starts of runs of equal (h_0, h_2).
       const unsigned rl = lane < mt.nb ? rs[lane] : 0u;
       const int bl = (int)((rl >> 3) & 7);
-      unsigned mask = __ballot_sync(~0u, (rl & RES_REGULAR) && bl <= wb_hi && bl + W - 1 >= wb_lo);
-      const unsigned kl = rl & 0x1c7u;
+      const bool hit = (rl & RES_REGULAR) && bl <= wb_hi && bl + W - 1 >= wb_lo;
+      unsigned mask = __ballot_sync(~0u, hit);
+      // runs: consecutive hit nodes of equal (h_0, h_2) (other nodes get a key no run has)
+      const unsigned kl = hit ? (rl & 0x1c7u) : 0xffffffffu;
       const unsigned kup = __shfl_up_sync(~0u, kl, 1);
       const unsigned rstart = __ballot_sync(~0u, lane == 0 || kl != kup);
       while (mask) {
