@@ -225,6 +225,26 @@ __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, 
 #pragma unroll
       for (int t = 0; t < WF; ++t) w2r[t] = (R)wl[t];
       const C* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
+      if constexpr (TEAM == WF) {
+        // lane tl walks the WF rows (t0, tl), t0 = 0 .. WF-1: its dim-1
+        // factor is fixed and the row pointer advances by one halo plane --
+        // no per-row index arithmetic, one factor load less per row
+        const R f1 = (R)w1[o1 + tl];
+        const C* row = corner + tl * HS;
+#pragma unroll 2
+        for (int t0 = 0; t0 < WF; ++t0, row += H1 * HS) {
+          R sre = 0, sim = 0;
+#pragma unroll
+          for (int t = 0; t < WF; ++t) {
+            C v = row[t];
+            sre = fma(w2r[t], v.x, sre);
+            sim = fma(w2r[t], v.y, sim);
+          }
+          R w01 = (R)(w0[o0 + t0] * f1);
+          are = fma(w01, sre, are);
+          aim = fma(w01, sim, aim);
+        }
+      } else
 #pragma unroll 2
       for (int p = tl; p < WF * WF; p += TEAM) {
         int t0 = p / WF, t1 = p - t0 * WF;
