@@ -450,10 +450,10 @@ int32_t nfftk_get_params(int32_t h, int64_t* out, int32_t count) {
   Plan* p = e->plan;
   const bool tensor = p->ready && p->mode == MODE_TENSOR && p->d <= MAX_D;
   const int path = !tensor ? 0 : (res_ok(p->geom) ? 2 : (pipe_geometry(p->geom) ? 1 : 0));
-  int64_t v[15] = {p->d, p->M, p->m, p->window, p->single ? 1 : 0, (int64_t)p->f1, (int64_t)p->f2,
+  int64_t v[16] = {p->d, p->M, p->m, p->window, p->single ? 1 : 0, (int64_t)p->f1, (int64_t)p->f2,
                    p->has_nodes, p->ready, p->mode, p->ntiles, p->nsubs, (int64_t)p->width_sum,
-                   path, p->geom.nwide};
-  for (int i = 0; i < count && i < 15; ++i) out[i] = v[i];
+                   path, p->geom.nwide, p->ready && p->fft3 ? 1 : 0};
+  for (int i = 0; i < count && i < 16; ++i) out[i] = v[i];
   return 0;
 }
 

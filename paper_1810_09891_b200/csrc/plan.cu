@@ -137,6 +137,7 @@ Plan::~Plan() {
   cudaFree(cols);
   if (!grid_external) cudaFree(grid);
   cudaFree(gp);
+  for (int i = 0; i < MAX_D; ++i) cudaFree(fft_tw[i]);
   cudaFree(sched);
   for (auto& h : hgraph)
     if (h.exec) cudaGraphExecDestroy(h.exec);
@@ -539,6 +540,16 @@ static void build_tensor_map(Plan* p) {
   p->tmap_ready = true;
 }
 
+static void ensure_cufft(Plan* p) {
+  if (p->fft_ready) return;
+  int nn[MAX_D];
+  for (int i = 0; i < p->d; ++i) nn[i] = p->n[i];
+  cufftResult r = cufftPlanMany(&p->fft, p->d, nn, nullptr, 1, 0, nullptr, 1, 0,
+                                p->single ? CUFFT_C2C : CUFFT_Z2Z, 1);
+  if (r != CUFFT_SUCCESS) fail(EK_CUDA, "cufftPlanMany failed (" + std::to_string((int)r) + ")");
+  p->fft_ready = true;
+}
+
 static void ensure_grid(Plan* p) {
   if (!p->grid) NFFTK_CUDA(cudaMalloc(&p->grid, p->elem_bytes() * p->grid_size));
   if (!p->sched) {
@@ -559,13 +570,32 @@ static void ensure_grid(Plan* p) {
     }
   }
   if (!p->tmap_ready) build_tensor_map(p);
-  if (!p->fft_ready) {
-    int nn[MAX_D];
-    for (int i = 0; i < p->d; ++i) nn[i] = p->n[i];
-    cufftResult r = cufftPlanMany(&p->fft, p->d, nn, nullptr, 1, 0, nullptr, 1, 0,
-                                  p->single ? CUFFT_C2C : CUFFT_Z2Z, 1);
-    if (r != CUFFT_SUCCESS) fail(EK_CUDA, "cufftPlanMany failed (" + std::to_string((int)r) + ")");
-    p->fft_ready = true;
+  // pruned F / F^H (fft.cu) where the geometry allows it and its two
+  // intermediate arrays fit the dense grid buffer (the trafo's scratch)
+  p->fft3 = p->d == 3 && fft3_supported(p->d, p->n.data(), p->N.data(), p->single);
+  if (p->fft3) {
+    for (int i = 0; i < 3; ++i) {
+      p->fq.N[i] = p->N[i];
+      p->fq.n[i] = p->n[i];
+      p->fq.np[i] = p->geom.np[i];
+    }
+    if (fft3_scratch_elems(p->fq) > (size_t)p->grid_size) p->fft3 = false;
+  }
+  if (p->fft3) {
+    p->fq.m = p->m;
+    p->fq.grid_size = (double)p->grid_size;
+    for (int i = 0; i < 3; ++i) {
+      if (!p->fft_tw[i]) {
+        std::vector<unsigned char> tw;
+        fft3_twiddles(p->n[i], p->single, tw);
+        NFFTK_CUDA(cudaMalloc(&p->fft_tw[i], tw.size()));
+        NFFTK_CUDA(cudaMemcpy(p->fft_tw[i], tw.data(), tw.size(), cudaMemcpyHostToDevice));
+      }
+      p->fq.tw[i] = p->fft_tw[i];
+      p->fq.icol[i] = p->dq.icol[i];
+    }
+  } else {
+    ensure_cufft(p);
   }
 }
 
@@ -673,6 +703,7 @@ static void count_evals(Plan* p) {
 
 static void exec_fft(Plan* p, int dir, cudaStream_t s) {
   NFFTK_CUDA(cudaGetLastError());
+  ensure_cufft(p);
   if (cufftSetStream(p->fft, s) != CUFFT_SUCCESS) fail(EK_CUDA, "cufftSetStream failed");
   cufftResult r = p->single ? cufftExecC2C(p->fft, (cufftComplex*)p->grid, (cufftComplex*)p->grid, dir)
                             : cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->grid,
@@ -696,6 +727,16 @@ void plan_interp_device(Plan* p, void* f, cudaStream_t s) {
 void plan_trafo_device(Plan* p, const void* fhat, void* f, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
+  if (p->fft3) {
+    // D, F and the ghost padding in three pruned passes: f_hat -> (scratch in
+    // the dense grid buffer) -> the padded grid the gather reads
+    { PhaseScope ps(p, PH_FFT_FWD, s); fft3_forward(p->single, fhat, p->grid, p->gp, true, p->fq, s); }
+    { PhaseScope ps(p, PH_INTERP, s);
+      launch_interp(p->single, p->tmap, p->gp, f, p->xs, p->perm, p->subs, p->nsubs, p->geom, s); }
+    NFFTK_CUDA(cudaGetLastError());
+    count_evals(p);
+    return;
+  }
   { PhaseScope ps(p, PH_DECONV, s); launch_deconv(p->single, fhat, p->grid, p->dq, s); }
   { PhaseScope ps(p, PH_FFT_FWD, s); exec_fft(p, CUFFT_FORWARD, s); }
   plan_interp_device(p, f, s);
@@ -731,6 +772,13 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
 void plan_adjoint_finish_device(Plan* p, void* fhat, cudaStream_t s) {
   require_ready(p);
   NFFTK_CUDA(cudaSetDevice(p->device));
+  if (p->fft3) {
+    // F^H, the pack and D^H in three pruned passes; the padded grid buffer
+    // (idle during the adjoint) and then the dense grid itself are scratch
+    { PhaseScope ps(p, PH_FFT_INV, s); fft3_inverse(p->single, p->grid, p->gp, p->grid, fhat, p->fq, s); }
+    NFFTK_CUDA(cudaGetLastError());
+    return;
+  }
   { PhaseScope ps(p, PH_FFT_INV, s); exec_fft(p, CUFFT_INVERSE, s); }
   { PhaseScope ps(p, PH_PACK, s); launch_pack(p->single, p->grid, fhat, p->dq, s); }
   NFFTK_CUDA(cudaGetLastError());

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft.h"
 #include "kernels.h"
 
 namespace nfftk {
@@ -76,6 +77,11 @@ struct Plan {
   void* f_sorted = nullptr;         // spread input in tile-sorted order
   cufftHandle fft = 0;
   bool fft_ready = false;
+  // pruned three-pass F / F^H with D, D^H and the ghost padding fused in
+  // (fft.cu): d = 3 plans on power-of-two grids; cuFFT otherwise
+  bool fft3 = false;
+  Fft3Geom fq{};
+  void* fft_tw[MAX_D] = {nullptr, nullptr, nullptr};
 
   // ---- host ABI buffers (library-owned, zero-initialised; cabi.py:59-67)
   double* fhat_host = nullptr;

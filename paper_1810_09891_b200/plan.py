@@ -186,8 +186,8 @@ class Plan:
 
     # -- plumbing -------------------------------------------------------
     def _params(self):
-        out = (ctypes.c_int64 * 15)()
-        self._lib_checked().nfftk_get_params(self._h, out, 15)
+        out = (ctypes.c_int64 * 16)()
+        self._lib_checked().nfftk_get_params(self._h, out, 16)
         return list(out)
 
     def _lib_checked(self):
@@ -361,6 +361,13 @@ class Plan:
         (residue.cu spread + pipelined interp: d=3, m=4, 8^3 tiles), "pipe"
         (row-per-thread pipelined kernels) or "batch"."""
         return ("batch", "pipe", "residue")[int(self._params()[13])]
+
+    @property
+    def fft(self):
+        """Extension: how a ready plan runs F / F^H -- "pruned" (fft.cu: three
+        passes of line FFTs over the N-band only, with D, D^H and the ghost
+        padding fused in; d=3, power-of-two n) or "cufft" (dense n-grid)."""
+        return ("cufft", "pruned")[int(self._params()[15])]
 
     @property
     def wide_nodes(self):
