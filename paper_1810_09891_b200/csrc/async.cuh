@@ -51,6 +51,18 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                "r"(bytes));
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+#ifdef NFFTK_MBAR_HINT
+  // A/B: let a failed try_wait suspend the warp for up to the hinted time
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"((unsigned)NFFTK_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -60,6 +72,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {

@@ -38,9 +38,15 @@
 #include "fft.h"
 #include "kernels.h"
 
+#ifndef NFFTK_FFT_TW_LOADS
+#define NFFTK_FFT_TW_LOADS 1
+#endif
+
 namespace nfftk {
 
 namespace {
+
+constexpr bool FFT_HALF_GROUP = false;
 
 constexpr int fft_log2(int L) { return L <= 1 ? 0 : 1 + fft_log2(L / 2); }
 // radices: as many 8s as possible, the rest 4s (L = 2^p, p >= 6)
@@ -117,24 +123,52 @@ __device__ __forceinline__ int band_index(int e, int L, int N) {
   return e < h ? e + h : (e >= L - h ? e - L + h : -1);
 }
 
+// Lines per CTA.  Strided passes: lanes run across W = 128 / sizeof(complex)
+// adjacent lines (8 c128 / 16 c64: 128-byte global segments, one
+// shared-memory wavefront per lane group); G = W / 2 halves the CTA (more
+// CTAs per SM to overlap the load, butterfly and store phases) and skews the
+// element index by e / 8 so that the two elements a wavefront then covers
+// fall into different halves of a 128-byte bank row.  Contiguous pass: lanes
+// run along the line, G only sets the CTA size.
 template <typename R>
 struct FftCfg {
-  static constexpr int G = 16 / (int)sizeof(R);           // lines per CTA: 8 (c128) / 16 (c64): 128-byte segments
-  static constexpr int PS = sizeof(R) == 8 ? 3 : 4;       // contiguous pass: one pad element per 128 bytes
+  static constexpr int W = 64 / (int)sizeof(R);
+#ifndef NFFTK_FFT_GE_DIV
+#define NFFTK_FFT_GE_DIV 4
+#endif
+  static constexpr int GE = W / NFFTK_FFT_GE_DIV;         // contiguous pass: 2 (c128) / 4 (c64) lines per CTA
 };
 
-template <typename R, int L, bool EF>
-constexpr int fft_line_pitch() {
-  return EF ? L + (L >> FftCfg<R>::PS) : L;
+// contiguous pass: one pad element per 128 bytes (c64: per 16 elements when
+// the thread count per line allows it, see the kernel's index rules)
+template <typename R, int L>
+constexpr int fft_pad_shift() {
+  return sizeof(R) == 4 && L >= 128 ? 4 : 3;
 }
 
-// One pass: G lines per CTA, L / 8 threads per line.
-template <typename R, int L, int DIR, bool EF>
-__global__ void __launch_bounds__(FftCfg<R>::G* L / 8, (FftCfg<R>::G * L / 8 >= 128 ? 1024 / (FftCfg<R>::G * L / 8) : 8))
+template <typename R, int L, bool EF, int G>
+constexpr int fft_smem_elems() {
+  return EF ? G * (L + (L >> fft_pad_shift<R, L>())) : (G < FftCfg<R>::W ? (L + (L >> 3)) * G : L * G);
+}
+
+constexpr int fft_min_blocks(int threads) { return threads >= 128 ? 1024 / threads : 8; }
+
+// One pass: G lines per CTA, L / 8 threads per line.  Shared-memory index of
+// element e of line g: EF: g * pitch + e + (e >> PS) (one pad element per
+// 128 bytes); strided: e * G + g, or (e + (e >> 3)) * G + g for the half
+// group.  Every access below is base + compile-time offset: reads are at
+// e = j + c T, writes at e = d0 + r Ns (Ns >= 8) or 8 j + r, and the pad term
+// of such a sum splits into the pad terms of its parts (no carry between
+// them).
+template <typename R, int L, int DIR, bool EF, int G>
+__global__ void __launch_bounds__(G* L / 8, fft_min_blocks(G* L / 8))
 k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPass q) {
   using C = cplx_t<R>;
-  constexpr int G = FftCfg<R>::G, T = L / 8, PS = FftCfg<R>::PS;
+  constexpr int T = L / 8;
+  constexpr int PS = fft_pad_shift<R, L>();
+  constexpr bool SKEW = !EF && G < FftCfg<R>::W;
   constexpr int NS = fft_stages(L);
+  constexpr bool LAST4 = fft_radix(L, NS - 1) == 4;
   extern __shared__ __align__(16) unsigned char fft_smem[];
   C* buf = reinterpret_cast<C*>(fft_smem);
   const C* __restrict__ tw = reinterpret_cast<const C*>(q.tw);
@@ -142,21 +176,29 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
   const int j = EF ? (int)threadIdx.x % T : (int)threadIdx.x / G;
   const int nvb = q.nv / G;
   const int u = (int)(blockIdx.x / nvb), v = (int)(blockIdx.x % nvb) * G + g;
-  auto sidx = [&](int e) -> int { return EF ? g * fft_line_pitch<R, L, true>() + e + (e >> PS) : e * G + g; };
+  // index of element e of this thread's line / offset of an element step c
+  auto sidx = [&](int e) -> int {
+    return EF ? g * (L + (L >> PS)) + e + (e >> PS) : (SKEW ? (e + (e >> 3)) * G + g : e * G + g);
+  };
+  auto step = [](int c) -> int { return EF ? c + (c >> PS) : (SKEW ? (c + (c >> 3)) * G : c * G); };
 
   C x[8];
   // ---- stage 0: radix 8 straight from global memory (zero outside the band)
   {
     const C* src = in + (int64_t)u * q.in_su + (int64_t)v * q.in_sv;
+    const int se = (int)q.in_se;
     double fac = 1.0;
     if (q.scale_in) fac = q.scale * q.col_u[u] * q.col_v[v];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int e = j + r * T;
-      const int k = q.in_band ? band_index(e, L, q.in_band) : e;
+      // band groups: q.in_off[r] is the compact index of element r T (the
+      // band edges fall on multiples of T), -1 outside, -2: test per element
+      int k = q.in_off[r];
+      if (k == -2) k = band_index(j + r * T, L, q.in_band);
+      else if (k >= 0) k += j;
       C val = C{0, 0};
       if (k >= 0) {
-        val = src[(int64_t)k * q.in_se];
+        val = src[k * se];
         if (q.scale_in) {
           const double f = fac * q.col_e[k];
           val.x = (R)((double)val.x * f);
@@ -166,55 +208,82 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
       x[r] = val;
     }
     butterfly<R, DIR, 8>(x);
+    C* w0 = buf + sidx(8 * j);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) buf[sidx(j * 8 + r)] = x[r];
+    for (int r = 0; r < 8; ++r) w0[r * (EF ? 1 : G)] = x[r];
   }
   __syncthreads();
+  const C* rd = buf + sidx(j);
   // ---- middle and last stages
   int Ns = 8;
 #pragma unroll
   for (int s = 1; s < NS; ++s) {
-    constexpr int dummy = 0;
-    (void)dummy;
     const int RAD = fft_radix(L, s);
     const bool last = s == NS - 1;
     if (RAD == 8) {
       const int k = j & (Ns - 1);
-      const int tstep = k * (L / (Ns * 8));
+      const C* tp = tw + k * (L / (Ns * 8));
+      const int ts = k * (L / (Ns * 8));
 #pragma unroll
-      for (int r = 0; r < 8; ++r) x[r] = buf[sidx(j + r * T)];
+      for (int r = 0; r < 8; ++r) x[r] = rd[step(r * T)];
+#if NFFTK_FFT_TW_LOADS == 3
+      {
+        // three twiddle loads (w, w^2, w^4), the other powers by products:
+        // the passes are bound by the load/store unit, not by the FP64 pipe
+        C w1 = tp[0], w2 = tp[ts], w4 = tp[3 * ts];
+        if (DIR > 0) { w1.y = -w1.y; w2.y = -w2.y; w4.y = -w4.y; }
+        const C w3 = Cx<R>::mul(w1, w2), w5 = Cx<R>::mul(w1, w4), w6 = Cx<R>::mul(w2, w4);
+        const C w7 = Cx<R>::mul(w3, w4);
+        x[1] = Cx<R>::mul(x[1], w1); x[2] = Cx<R>::mul(x[2], w2); x[3] = Cx<R>::mul(x[3], w3);
+        x[4] = Cx<R>::mul(x[4], w4); x[5] = Cx<R>::mul(x[5], w5); x[6] = Cx<R>::mul(x[6], w6);
+        x[7] = Cx<R>::mul(x[7], w7);
+      }
+#elif NFFTK_FFT_TW_LOADS == 1
+      {
+        // one twiddle load, the powers by products (default): the passes are
+        // bound by the load/store unit -- C5 F + F^H 3.20 ms with seven loads
+        // per stage, 2.65 with three, 2.38 with one; the rounding of the
+        // products adds ~1e-16 to the transform's relative error
+        C w1 = tp[0];
+        if (DIR > 0) w1.y = -w1.y;
+        const C w2 = Cx<R>::mul(w1, w1), w3 = Cx<R>::mul(w1, w2), w4 = Cx<R>::mul(w2, w2);
+        const C w5 = Cx<R>::mul(w1, w4), w6 = Cx<R>::mul(w2, w4), w7 = Cx<R>::mul(w3, w4);
+        x[1] = Cx<R>::mul(x[1], w1); x[2] = Cx<R>::mul(x[2], w2); x[3] = Cx<R>::mul(x[3], w3);
+        x[4] = Cx<R>::mul(x[4], w4); x[5] = Cx<R>::mul(x[5], w5); x[6] = Cx<R>::mul(x[6], w6);
+        x[7] = Cx<R>::mul(x[7], w7);
+      }
+#else
 #pragma unroll
       for (int r = 1; r < 8; ++r) {
-        C w = tw[tstep * r];
+        C w = tp[ts * (r - 1)];
         if (DIR > 0) w.y = -w.y;
         x[r] = Cx<R>::mul(x[r], w);
       }
+#endif
       butterfly<R, DIR, 8>(x);
-      const int d0 = (j / Ns) * Ns * 8 + k;
       if (!last) {
+        C* wr = buf + sidx((j / Ns) * Ns * 8 + k);
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 8; ++r) buf[sidx(d0 + r * Ns)] = x[r];
+        for (int r = 0; r < 8; ++r) wr[step(r * Ns)] = x[r];
         __syncthreads();
       }
-      // last stage: x[r] is element d0 + r * Ns = j + r * T (Ns = T)
+      // last stage (Ns = T): x[r] is element j + r T
     } else {
       // radix 4: two butterflies per thread, jj = j and j + T; values 4 q + r
 #pragma unroll
-      for (int qq = 0; qq < 2; ++qq) {
-        const int jj = j + qq * T;
+      for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) x[4 * qq + r] = buf[sidx(jj + r * (L / 4))];
-      }
+        for (int r = 0; r < 4; ++r) x[4 * qq + r] = rd[step(qq * T + r * (L / 4))];
       int d0[2];
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq) {
         const int jj = j + qq * T;
         const int k = jj & (Ns - 1);
-        const int tstep = k * (L / (Ns * 4));
+        const int ts = k * (L / (Ns * 4));
 #pragma unroll
         for (int r = 1; r < 4; ++r) {
-          C w = tw[tstep * r];
+          C w = tw[ts * r];
           if (DIR > 0) w.y = -w.y;
           x[4 * qq + r] = Cx<R>::mul(x[4 * qq + r], w);
         }
@@ -224,25 +293,29 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
       if (!last) {
         __syncthreads();
 #pragma unroll
-        for (int qq = 0; qq < 2; ++qq)
+        for (int qq = 0; qq < 2; ++qq) {
+          C* wr = buf + sidx(d0[qq]);
 #pragma unroll
-          for (int r = 0; r < 4; ++r) buf[sidx(d0[qq] + r * Ns)] = x[4 * qq + r];
+          for (int r = 0; r < 4; ++r) wr[step(r * Ns)] = x[4 * qq + r];
+        }
         __syncthreads();
       }
       // last stage (Ns = L / 4): x[4 q + r] is element j + q T + r L / 4
     }
     Ns *= RAD;
   }
-  // ---- store: element index of x[i]
-  constexpr bool LAST4 = fft_radix(L, NS - 1) == 4;
-  double fac = 1.0;
-  if (q.scale_out) fac = q.scale * q.col_u[u] * q.col_v[v];
+  // ---- store: x[i] is element j + EOFF(i)
+#define NFFTK_EOFF(i) (LAST4 ? ((i) >> 2) * T + ((i)&3) * (L / 4) : (i)*T)
   if (q.pad_m < 0) {
     C* dst = out + (int64_t)u * q.out_su + (int64_t)v * q.out_sv;
+    const int se = (int)q.out_se;
+    double fac = 1.0;
+    if (q.scale_out) fac = q.scale * q.col_u[u] * q.col_v[v];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int e = LAST4 ? j + (i >> 2) * T + (i & 3) * (L / 4) : j + i * T;
-      const int k = q.out_band ? band_index(e, L, q.out_band) : e;
+      int k = q.out_off[NFFTK_EOFF(i) / T];
+      if (k == -2) k = band_index(j + NFFTK_EOFF(i), L, q.out_band);
+      else if (k >= 0) k += j;
       if (k < 0) continue;
       C val = x[i];
       if (q.scale_out) {
@@ -250,61 +323,88 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
         val.x = (R)((double)val.x * f);
         val.y = (R)((double)val.y * f);
       }
-      dst[(int64_t)k * q.out_se] = val;
+      dst[k * se] = val;
     }
   } else {
     // ghost-padded grid: slot s of a dim sits at padded index s + m + k n for
     // every k that lands inside [0, np) (kernels.cu k_pad); u, v are the
     // slots of dims 0 and 1, the line runs along dim 2
-    const int m = q.pad_m;
-    for (int ka = -1; ka <= 1; ++ka) {
-      const int pa = u + m + ka * q.pad_n[0];
-      if (pa < 0 || pa >= q.pad_np[0]) continue;
-      for (int kb = -1; kb <= 1; ++kb) {
-        const int pb = v + m + kb * q.pad_n[1];
-        if (pb < 0 || pb >= q.pad_np[1]) continue;
-        C* row = out + ((int64_t)pa * q.pad_np[1] + pb) * q.pad_np[2];
+    const int m = q.pad_m, np2 = q.pad_np[2];
+    auto put_row = [&](C* row) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = LAST4 ? j + (i >> 2) * T + (i & 3) * (L / 4) : j + i * T;
-          const int pc = e + m;
-          row[pc] = x[i];
-          if (pc - L >= 0) row[pc - L] = x[i];
-          if (pc + L < q.pad_np[2]) row[pc + L] = x[i];
+      for (int i = 0; i < 8; ++i) {
+        const int pc = j + NFFTK_EOFF(i) + m;
+        row[pc] = x[i];
+        // images along the line: only its first and last cells have any
+        if (NFFTK_EOFF(i) + T + m > L && pc >= L) row[pc - L] = x[i];
+        if (NFFTK_EOFF(i) + m + L < np2 && pc + L < np2) row[pc + L] = x[i];
+      }
+    };
+    put_row(out + ((int64_t)(u + m) * q.pad_np[1] + (v + m)) * np2);
+    // image rows: slots within m (+2) of the edge of dims 0, 1
+    const bool ia = u + m >= q.pad_n[0] || u + m + q.pad_n[0] < q.pad_np[0];
+    const bool ib = v + m >= q.pad_n[1] || v + m + q.pad_n[1] < q.pad_np[1];
+    if (ia || ib) {
+      for (int ka = -1; ka <= 1; ++ka) {
+        const int pa = u + m + ka * q.pad_n[0];
+        if (pa < 0 || pa >= q.pad_np[0]) continue;
+        for (int kb = -1; kb <= 1; ++kb) {
+          const int pb = v + m + kb * q.pad_n[1];
+          if (pb < 0 || pb >= q.pad_np[1] || (ka == 0 && kb == 0)) continue;
+          put_row(out + ((int64_t)pa * q.pad_np[1] + pb) * np2);
         }
       }
     }
   }
+#undef NFFTK_EOFF
 }
 
-template <typename R, int L, int DIR, bool EF>
+template <typename R, int L, int DIR, bool EF, int G>
 void launch_pass_t(const void* in, void* out, const FftPass& q, cudaStream_t s) {
-  constexpr int G = FftCfg<R>::G;
-  const size_t smem = sizeof(cplx_t<R>) * G * fft_line_pitch<R, L, EF>();
-  static bool attr = false;
-  if (!attr) {
-    NFFTK_CUDA(cudaFuncSetAttribute(k_fft_pass<R, L, DIR, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    attr = true;
-  }
+  const size_t smem = sizeof(cplx_t<R>) * fft_smem_elems<R, L, EF, G>();
+  NFFTK_CUDA(cudaFuncSetAttribute(k_fft_pass<R, L, DIR, EF, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
   const unsigned blocks = (unsigned)((int64_t)q.nu * (q.nv / G));
-  k_fft_pass<R, L, DIR, EF><<<blocks, G * L / 8, smem, s>>>((const cplx_t<R>*)in, (cplx_t<R>*)out, q);
+  k_fft_pass<R, L, DIR, EF, G><<<blocks, G * L / 8, smem, s>>>((const cplx_t<R>*)in, (cplx_t<R>*)out, q);
   count_launch();
+}
+
+// lines per CTA of the strided passes: NFFTK_FFT_G=full|half (A/B; default below)
+template <typename R>
+int strided_group() {
+  const char* e = getenv("NFFTK_FFT_G");
+  const bool half = e ? e[0] == 'h' : FFT_HALF_GROUP;
+  return half ? FftCfg<R>::W / 2 : FftCfg<R>::W;
+}
+
+template <typename R, int L, int DIR>
+void launch_pass_d(const void* in, void* out, const FftPass& q, bool ef, cudaStream_t s) {
+  constexpr int W = FftCfg<R>::W;
+  if (ef) launch_pass_t<R, L, DIR, true, FftCfg<R>::GE>(in, out, q, s);
+  else if (q.nv % W == 0 && strided_group<R>() == W) launch_pass_t<R, L, DIR, false, W>(in, out, q, s);
+  else launch_pass_t<R, L, DIR, false, W / 2>(in, out, q, s);
 }
 
 template <typename R, int L>
 void launch_pass_l(const void* in, void* out, const FftPass& q, int dir, bool ef, cudaStream_t s) {
-  if (dir < 0) {
-    if (ef) launch_pass_t<R, L, -1, true>(in, out, q, s);
-    else launch_pass_t<R, L, -1, false>(in, out, q, s);
-  } else {
-    if (ef) launch_pass_t<R, L, 1, true>(in, out, q, s);
-    else launch_pass_t<R, L, 1, false>(in, out, q, s);
+  if (dir < 0) launch_pass_d<R, L, -1>(in, out, q, ef, s);
+  else launch_pass_d<R, L, 1>(in, out, q, ef, s);
+}
+
+static void band_groups(int L, int band, int* off) {
+  const int T = L / 8, h = band / 2;
+  for (int c = 0; c < 8; ++c) {
+    if (!band) off[c] = c * T;
+    else if (h % T) off[c] = -2;
+    else off[c] = (c + 1) * T <= h ? c * T + h : (c * T >= L - h ? c * T - L + h : -1);
   }
 }
 
 template <typename R>
-void launch_pass(const void* in, void* out, const FftPass& q, int L, int dir, bool ef, cudaStream_t s) {
+void launch_pass(const void* in, void* out, const FftPass& q0, int L, int dir, bool ef, cudaStream_t s) {
+  FftPass q = q0;
+  band_groups(L, q.in_band, q.in_off);
+  band_groups(L, q.out_band, q.out_off);
   switch (L) {
     case 64: launch_pass_l<R, 64>(in, out, q, dir, ef, s); break;
     case 128: launch_pass_l<R, 128>(in, out, q, dir, ef, s); break;
@@ -324,7 +424,7 @@ bool len_ok(int L) { return L == 64 || L == 128 || L == 256 || L == 512; }
 bool fft3_supported(int d, const int* n, const int* N, bool single) {
   if (getenv("NFFTK_NO_PRUNED_FFT")) return false;
   if (d != 3) return false;
-  const int G = single ? 16 : 8;
+  const int G = single ? 8 : 4;  // the half group of the strided passes
   for (int i = 0; i < 3; ++i)
     if (!len_ok(n[i]) || (N[i] & 1) || N[i] > n[i] || N[i] < 2) return false;
   return N[2] % G == 0 && n[1] % G == 0;

@@ -17,6 +17,10 @@ struct FftPass {
   int64_t in_su, in_sv, in_se;
   int64_t out_su, out_sv, out_se;
   int in_band, out_band;
+  // per group of L / 8 elements (element c L / 8 onwards): compact index of
+  // its first element, -1 = outside the band, -2 = edge inside the group
+  // (test per element); filled by the launcher
+  int in_off[8], out_off[8];
   int scale_in, scale_out;           // x scale col_u[u] col_v[v] col_e[idx] on load / store
   double scale;
   const double* col_e;
