@@ -222,8 +222,9 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
     const bool last = s == NS - 1;
     if (RAD == 8) {
       const int k = j & (Ns - 1);
-      const C* tp = tw + k * (L / (Ns * 8));
       const int ts = k * (L / (Ns * 8));
+      const C* tp = tw + ts;
+      (void)ts;
 #pragma unroll
       for (int r = 0; r < 8; ++r) x[r] = rd[step(r * T)];
 #if NFFTK_FFT_TW_LOADS == 3

@@ -2187,7 +2187,7 @@ void launch_spread(bool single, void* gp, const void* f, void* fs, const double*
                    const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if (nsubs <= 0) return;
   if (res_ok(g)) {  // gp: the dense grid (dense_flush)
-    launch_spread_res(single, gp, fs, xs, subs, nsubs, g, s);
+    launch_spread_res(single, gp, fs, f, perm, xs, subs, nsubs, g, s);
     return;
   }
   const CUtensorMap* tm = nullptr;

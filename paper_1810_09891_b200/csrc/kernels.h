@@ -42,8 +42,9 @@ void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, unsigned*
 // residue-owned d = 3 spread (residue.cu)
 bool res_geometry(const Geom& g, bool single);
 bool res_ok(const Geom& g);
-void launch_spread_res(bool single, void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
-                       const Geom& g, cudaStream_t s);
+bool res_gathers(const Geom& g, bool single);
+void launch_spread_res(bool single, void* grid, const void* fs, const void* f, const int* perm, const double* xs,
+                       const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
 
 void lex_order(const double* x_dev, int64_t M, const Geom& g, int* order, cudaStream_t s);
 void psi_reference(const double* x_dev, int64_t M, const Geom& g, double* psi, double* vals, int64_t* idx,

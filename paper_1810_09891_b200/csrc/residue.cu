@@ -77,7 +77,7 @@ struct AresCfg {
   static constexpr size_t SB = W_BYTES + R_BYTES + F_BYTES;
   static constexpr size_t RING_OFF = ROWS_BYTES;
   static constexpr size_t CTL_OFF = RING_OFF + S * SB;
-  static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 48);
+  static constexpr size_t SMEM = CTL_OFF + al(16 * (size_t)S + sizeof(AresMeta) * S + 64);
 };
 
 // the W last-dim factors of a node (16-byte loads for fp64 rows, 8-byte for fp32 rows)
@@ -137,9 +137,10 @@ __device__ __forceinline__ void load_factors(const R* w, R* o) {
     } while (--cnt);                     \
   } break;
 
-template <typename R, int MM, int NB, int S, int BLOCKS>
+template <typename R, int MM, int NB, int S, int BLOCKS, bool GATHER>
 __global__ void __launch_bounds__((AresCfg<R, MM, NB, S>::THREADS), BLOCKS)
 k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted,
+             const cplx_t<R>* __restrict__ funs, const int* __restrict__ perm,
              const R* __restrict__ psi, const unsigned* __restrict__ rrec,
              const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
@@ -155,7 +156,15 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL_OFF);
   unsigned long long* empty = full + S;
   AresMeta* meta = reinterpret_cast<AresMeta*>(empty + S);
-  int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk, next sub
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: sub, base, end, tile, pk, next sub, last batch: nodes, slot
+  // Sample gather (GATHER): the samples are not read from a
+  // sorted copy (k_permute_samples: one more pass over f) but fetched by warp
+  // 0 straight from the caller's array, lane l bringing sample
+  // funs[perm[base + l]] of the batch with a 16- / 8-byte cp.async whose completion
+  // arrives on the batch's mbarrier (32 lane arrivals + the producer's);
+  // the lane loads its index one batch ahead.
+  constexpr bool gather = GATHER;
+  static_assert(!GATHER || NB == 32, "gather: one sample per lane of warp 0");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   C* const myrow = reinterpret_cast<C*>(smem) + (size_t)threadIdx.x * P::RS;  // this lane's staging row
   // pst[5] is the subproblem after pst[0], drawn one ahead so that its node
@@ -173,7 +182,8 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       if (nx < nsubs) {
         const int4 sn = subs[nx];
         l2_prefetch(psi + (int64_t)sn.y * PR, (unsigned)(sizeof(R) * PR) * (unsigned)sn.z);
-        l2_prefetch(fsorted + (sn.y & ~1), (unsigned)sizeof(C) * (unsigned)((sn.z + 2) & ~1));
+        if (gather) l2_prefetch(perm + (sn.y & ~3), 4u * (unsigned)((sn.z + 6) & ~3));
+        else l2_prefetch(fsorted + (sn.y & ~1), (unsigned)sizeof(C) * (unsigned)((sn.z + 2) & ~1));
         l2_prefetch(rrec + (sn.y & ~3), 4u * (unsigned)((sn.z + 6) & ~3));
       }
     }
@@ -184,6 +194,10 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
     AresMeta* mt = meta + slot;
     pst[4] = pk + 1;
+    if (gather) {
+      pst[6] = 0;
+      pst[7] = slot;
+    }
     if (pst[0] >= nsubs) {
       mt->nb = -1;
       mbar_arrive(full + slot);
@@ -201,32 +215,61 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     mt->off = off;
     unsigned char* st = smem + P::RING_OFF + slot * P::SB;
     const unsigned wb = (unsigned)(sizeof(R) * PR) * nb, rb = 4u * rcnt,
-                   fb = (unsigned)P::ELEM * ((nb + foff + FA - 1) & ~(FA - 1));
+                   fb = gather ? 0u : (unsigned)P::ELEM * ((nb + foff + FA - 1) & ~(FA - 1));
     mbar_expect_tx(full + slot, wb + rb + fb);
+    if (gather) pst[6] = nb;
 #ifdef NFFTK_NO_STREAM_HINT
     bulk_g2s(st, psi + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot);
-    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (!gather) bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
 #else
     const unsigned long long pol = l2_evict_first_policy();
     bulk_g2s_stream(st, psi + (int64_t)pbase * PR, wb, full + slot, pol);
     bulk_g2s_stream(st + P::W_BYTES, rrec + (pbase - off), rb, full + slot, pol);
-    bulk_g2s_stream(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot, pol);
+    if (!gather) bulk_g2s_stream(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot, pol);
 #endif
     if (pbase + nb < pend) pst[1] = pbase + nb;
     else load_sub(pst[5]);
   };
+  // warp 0: index of this lane's sample in the batch the producer state points at
+  auto fetch_idx = [&]() -> int {
+    const int b = pst[1] + lane;
+    return pst[0] < nsubs && b < pst[2] ? perm[b] : 0;
+  };
+  int pidx = 0;
+  // warp 0, converged: post the next batch; in gather mode every lane then
+  // sends its sample after the batch's byte count is posted
+  auto produce_w = [&]() {
+    if (gather) __syncwarp();
+    if (lane == 0) produce();
+    if (gather) {
+      __syncwarp();
+      const int slot = pst[7];
+      if (lane < pst[6])
+        cp_async_cell<C>(reinterpret_cast<C*>(smem + P::RING_OFF + slot * P::SB + P::W_BYTES + P::R_BYTES) + lane,
+                         funs + pidx);
+      cp_async_arrive_noinc(full + slot);
+      pidx = fetch_idx();
+    }
+  };
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(full + i, 1);
+      mbar_init(full + i, gather ? 33 : 1);
       mbar_init(empty + i, NW);
     }
     pst[4] = 0;
     load_sub((int)blockIdx.x);
   }
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int i = 0; i < S - 1; ++i) produce();
+  if constexpr (GATHER) {
+    if (warp == 0) {
+      pidx = fetch_idx();
+      for (int i = 0; i < S - 1; ++i) produce_w();
+    }
+  } else {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < S - 1; ++i) produce();
+  }
 
   R accr[H], acci[H];
 #pragma unroll
@@ -277,7 +320,8 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       const unsigned char* st = smem + P::RING_OFF + slot * P::SB;
       const R* ws = reinterpret_cast<const R*>(st);
       const unsigned* rs = reinterpret_cast<const unsigned*>(st + P::W_BYTES) + mt.off;
-      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (P::FA > 1 ? (mt.off & (P::FA - 1)) : 0);
+      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) +
+                    (P::FA > 1 && !gather ? (mt.off & (P::FA - 1)) : 0);
       // Per-batch warp view: lane l holds node l's record; one ballot gives
       // the regular nodes whose dim-1 window meets this warp's b values,
       // another the starts of runs of equal (h_0, h_2).
@@ -321,7 +365,11 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
-      if (threadIdx.x == 0) produce();
+      if constexpr (GATHER) {
+        if (warp == 0) produce_w();
+      } else {
+        if (threadIdx.x == 0) produce();
+      }
       if (mt.last) {
         ++k;
         break;
@@ -340,8 +388,8 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
 // lanes, atomics into the dense grid.
 template <typename R>
 __global__ void __launch_bounds__(256)
-k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, const unsigned* __restrict__ rrec,
-             const double* __restrict__ xs, Geom g) {
+k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, const cplx_t<R>* __restrict__ funs,
+             const int* __restrict__ perm, const unsigned* __restrict__ rrec, const double* __restrict__ xs, Geom g) {
   using C = cplx_t<R>;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -368,7 +416,7 @@ k_wide_nodes(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fs, con
         for (int dim = 0; dim < 3; ++dim)
           if (lane < wd[dim]) fac[dim] = dim_factor(g, dim, xs[dim * g.M + j], lo[dim] + lane) * g.wscale[dim];
       }
-      const C fj = fs[j];
+      const C fj = perm ? funs[perm[j]] : fs[j];
       const int cells = wd[0] * wd[1] * wd[2];
       for (int q0 = 0; q0 < cells; q0 += 32) {
         const int q = q0 + lane;
@@ -420,26 +468,40 @@ static int sm_count() {
   return sms;
 }
 
-template <typename R, int MM, int NB, int S, int BLOCKS>
-static void spread_res_go(void* grid, const void* fs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+template <typename R, int MM, int NB, int S, int BLOCKS, bool GATHER>
+static void spread_res_gg(void* grid, const void* fs, const void* funs, const int* perm, const int4* subs, int nsubs,
+                          const Geom& g, cudaStream_t s) {
   using P = AresCfg<R, MM, NB, S>;
   static_assert(P::SMEM <= 227 * 1024, "residue spread: shared memory");
   if (g.psi_pad != (P::STEN3 ? 2 : 1) || (g.psi_f32 != 0) != (sizeof(R) == 4))
     fail(EK_CUDA, "residue spread: PRE_PSI layout mismatch");
-  auto kern = k_spread_res<R, MM, NB, S, BLOCKS>;
+  auto kern = k_spread_res<R, MM, NB, S, BLOCKS, GATHER>;
   NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
   int per_sm = 0;
   NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
   const int grid_x = std::max(1, std::min(nsubs, sm_count() * std::max(1, per_sm)));
   Geom q = g;
   if ((int64_t)nsubs < 4LL * grid_x) q.sched = nullptr;  // static order (gridding.cu sched_geom)
-  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)grid, (const cplx_t<R>*)fs, (const R*)g.psi, g.rrec, subs,
-                                          nsubs, q);
+  kern<<<grid_x, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)grid, (const cplx_t<R>*)fs, (const cplx_t<R>*)funs, perm,
+                                          (const R*)g.psi, g.rrec, subs, nsubs, q);
   count_launch();
 }
 
+template <typename R, int MM, int NB, int S, int BLOCKS>
+static void spread_res_go(void* grid, const void* fs, const void* funs, const int* perm, const int4* subs, int nsubs,
+                          const Geom& g, cudaStream_t s) {
+  if constexpr (NB == 32) {
+    if (perm) {
+      spread_res_gg<R, MM, NB, S, BLOCKS, true>(grid, fs, funs, perm, subs, nsubs, g, s);
+      return;
+    }
+  }
+  spread_res_gg<R, MM, NB, S, BLOCKS, false>(grid, fs, funs, perm, subs, nsubs, g, s);
+}
+
 template <typename R>
-static void spread_res_m(void* grid, const void* fs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+static void spread_res_m(void* grid, const void* fs, const void* funs, const int* perm, const int4* subs, int nsubs,
+                         const Geom& g, cudaStream_t s) {
   // ring shape / CTAs per SM.  m = 4, c128 (C5): batches of 32 on a 3-deep
   // ring measured best (20.4 ms; <16,3,5> 23.2, <16,4,4> 22.2, <32,2,4> 21.4,
   // <32,4,3> 23.4); NFFTK_RES_VARIANT keeps the others for A/B runs.  The
@@ -447,35 +509,47 @@ static void spread_res_m(void* grid, const void* fs, const int4* subs, int nsubs
   const char* e = getenv("NFFTK_RES_VARIANT");
   const int v = e ? atoi(e) : 0;
   switch (g.m) {
-    case 1: spread_res_go<R, 1, 32, 3, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 2: spread_res_go<R, 2, 32, 3, 4>(grid, fs, subs, nsubs, g, s); break;
-    case 3: spread_res_go<R, 3, 32, 3, 3>(grid, fs, subs, nsubs, g, s); break;
+    case 1: spread_res_go<R, 1, 32, 3, 4>(grid, fs, funs, perm, subs, nsubs, g, s); break;
+    case 2: spread_res_go<R, 2, 32, 3, 4>(grid, fs, funs, perm, subs, nsubs, g, s); break;
+    case 3: spread_res_go<R, 3, 32, 3, 3>(grid, fs, funs, perm, subs, nsubs, g, s); break;
     case 4:
-      if (v == 1) spread_res_go<R, 4, 16, 3, 5>(grid, fs, subs, nsubs, g, s);
-      else if (v == 2) spread_res_go<R, 4, 16, 4, 4>(grid, fs, subs, nsubs, g, s);
-      else if (v == 3) spread_res_go<R, 4, 32, 2, 4>(grid, fs, subs, nsubs, g, s);
-      else if (v == 4) spread_res_go<R, 4, 32, 4, 3>(grid, fs, subs, nsubs, g, s);
-      else spread_res_go<R, 4, 32, 3, 3>(grid, fs, subs, nsubs, g, s);
+      if (v == 1) spread_res_go<R, 4, 16, 3, 5>(grid, fs, funs, perm, subs, nsubs, g, s);
+      else if (v == 2) spread_res_go<R, 4, 16, 4, 4>(grid, fs, funs, perm, subs, nsubs, g, s);
+      else if (v == 3) spread_res_go<R, 4, 32, 2, 4>(grid, fs, funs, perm, subs, nsubs, g, s);
+      else if (v == 4) spread_res_go<R, 4, 32, 4, 3>(grid, fs, funs, perm, subs, nsubs, g, s);
+      else spread_res_go<R, 4, 32, 3, 3>(grid, fs, funs, perm, subs, nsubs, g, s);
       break;
-    case 5: spread_res_go<R, 5, 16, 3, 2>(grid, fs, subs, nsubs, g, s); break;
+    case 5: spread_res_go<R, 5, 16, 3, 2>(grid, fs, funs, perm, subs, nsubs, g, s); break;
     default:
-      if (v == 1) spread_res_go<R, 6, 32, 2, 1>(grid, fs, subs, nsubs, g, s);
-      else spread_res_go<R, 6, 16, 3, 2>(grid, fs, subs, nsubs, g, s);
+      if (v == 1) spread_res_go<R, 6, 32, 2, 1>(grid, fs, funs, perm, subs, nsubs, g, s);
+      else spread_res_go<R, 6, 16, 3, 2>(grid, fs, funs, perm, subs, nsubs, g, s);
       break;
   }
 }
 
 // B^H into the dense grid (zeroed by the caller): regular nodes by the
 // residue kernel, wide ones (g.nwide of them) by k_wide_nodes.
-void launch_spread_res(bool single, void* grid, const void* fs, const double* xs, const int4* subs, int nsubs,
-                       const Geom& g, cudaStream_t s) {
-  if (single) spread_res_m<float>(grid, fs, subs, nsubs, g, s);
-  else spread_res_m<double>(grid, fs, subs, nsubs, g, s);
+// the kernel gathers the samples itself (no sorted copy)
+bool res_gathers(const Geom& g, bool single) {
+  // (the ring shapes with 32-node batches: one sample per lane of warp 0)
+  (void)single;
+  return res_ok(g) && g.m <= 4 && !getenv("NFFTK_RES_VARIANT") && !getenv("NFFTK_NO_GATHER");
+}
+
+void launch_spread_res(bool single, void* grid, const void* fs, const void* funs, const int* perm_all,
+                       const double* xs, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+  const int* perm = res_gathers(g, single) ? perm_all : nullptr;
+  if (single) spread_res_m<float>(grid, fs, funs, perm, subs, nsubs, g, s);
+  else spread_res_m<double>(grid, fs, funs, perm, subs, nsubs, g, s);
   if (g.nwide > 0) {
     Geom q = g;
     q.mode = MODE_DIRECT;
-    if (single) k_wide_nodes<float><<<sm_count() * 4, 256, 0, s>>>((float2*)grid, (const float2*)fs, g.rrec, xs, q);
-    else k_wide_nodes<double><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (const double2*)fs, g.rrec, xs, q);
+    if (single)
+      k_wide_nodes<float><<<sm_count() * 4, 256, 0, s>>>((float2*)grid, (const float2*)fs, (const float2*)funs, perm,
+                                                         g.rrec, xs, q);
+    else
+      k_wide_nodes<double><<<sm_count() * 4, 256, 0, s>>>((double2*)grid, (const double2*)fs, (const double2*)funs,
+                                                          perm, g.rrec, xs, q);
     count_launch();
   }
 }

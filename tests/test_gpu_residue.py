@@ -155,3 +155,27 @@ def test_residue_matches_row_kernels(oracle, monkeypatch):
     assert q.gridding == "pipe"
     assert e2(q.trafo(fh), p.trafo(fh)) < 1e-13
     assert e2(q.adjoint(fs), p.adjoint(fs)) < 1e-13
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("kind,M", [("edges", 30000), ("dense", 3000), ("uniform", 33)])
+def test_residue_sample_gather_matches_sorted_copy(kind, M, precision, oracle, monkeypatch):
+    """Warp 0 gathers each batch's samples from the caller's array, one
+    cp.async per lane arriving on the batch's mbarrier (default);
+    NFFTK_NO_GATHER reads them from the sorted copy k_permute_samples makes.
+    Same FMA order per row: the adjoints agree to the rounding of the row
+    reductions, also across replays and with wide (k_wide_nodes) nodes."""
+    N, n = (16, 16, 16), (32, 32, 32)
+    x = nodes(n, M, seed=31, kind=kind)
+    rng = np.random.default_rng(13)
+    fs = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    monkeypatch.delenv("NFFTK_NO_GATHER", raising=False)
+    p = plan(N, n, x, monkeypatch, precision=precision)
+    a = [p.adjoint(fs) for _ in range(3)]
+    monkeypatch.setenv("NFFTK_NO_GATHER", "1")
+    b = p.adjoint(fs)
+    monkeypatch.delenv("NFFTK_NO_GATHER")
+    assert e2(oracle.adjoint(N, n, M4, x, fs), a[0]) < TOL[precision]
+    # the flushes are floating-point reductions whose order varies run to run
+    for v in a:
+        assert e2(b, v) < (1e-14 if precision == "double" else 1e-6)

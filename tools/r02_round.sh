@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/ncu_launch_summary.py gpurun_out/launches_C5.csv > gpurun_out/launches_C5_summary.txt 2>&1
 for c in ${PROFILE_CONFIGS:-C5}; do
   python tools/profile_config.py $c 1 > gpurun_out/prof_plain_$c.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:"k_(interp|spread)" -c 2 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_(interp|spread|fft_pass)" -c 8 \
       -o gpurun_out/full_$c python tools/profile_config.py $c 1 > gpurun_out/ncu_full_$c.log 2>&1
   python tools/ncu_summary.py gpurun_out/full_$c.ncu-rep > gpurun_out/ncu_full_$c.txt 2>&1
   python tools/ncu_traffic.py gpurun_out/full_$c.ncu-rep $c gpurun_out/ncu_traffic.json >> gpurun_out/ncu_full_$c.txt 2>&1
