@@ -1789,9 +1789,13 @@ struct Pipe2Cfg {
   static constexpr size_t SMEM = ROWS_OFF + al((size_t)H0 * HS * ELEM);
 };
 
-template <typename R, int MM, int T1>
+// GATHER: the samples are not read from a sorted copy but fetched by the
+// warp itself, lane l < NB bringing f[perm[base + l]] of the batch with one
+// cp.async that arrives on the batch's mbarrier (as in residue.cu).
+template <typename R, int MM, int T1, bool GATHER>
 __global__ void __launch_bounds__(32)
 k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
+               const cplx_t<R>* __restrict__ funs, const int* __restrict__ perm,
                const double* __restrict__ psi, const int4* __restrict__ rec,
                const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
@@ -1802,12 +1806,12 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
   unsigned long long* empty = full + S;
   StageMeta* meta = reinterpret_cast<StageMeta*>(empty + S);
-  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k, last batch: nodes, slot
   C* stage = reinterpret_cast<C*>(smem + P::ROWS_OFF);
   const int lane = threadIdx.x;
   if (lane == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(full + i, 1);
+      mbar_init(full + i, GATHER ? 33 : 1);
       mbar_init(empty + i, 1);
     }
     pst[0] = blockIdx.x;
@@ -1826,6 +1830,10 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
     StageMeta* mt = meta + slot;
     pst[4] = pk + 1;
+    if (GATHER) {
+      pst[5] = 0;
+      pst[6] = slot;
+    }
     if (pst[0] >= nsubs) {
       mt->nb = -1;
       mbar_arrive(full + slot);
@@ -1841,11 +1849,12 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     mt->foff = foff;
     unsigned char* st = smem + slot * P::SB;
     const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb,
-                   fb = (unsigned)sizeof(C) * fcnt;
+                   fb = GATHER ? 0u : (unsigned)sizeof(C) * fcnt;
     mbar_expect_tx(full + slot, wb + rb + fb);
+    if (GATHER) pst[5] = nb;
     bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
-    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (!GATHER) bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {
@@ -1859,8 +1868,29 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       }
     }
   };
-  if (lane == 0)
-    for (int i = 0; i < S - 1; ++i) produce();
+  // index of this lane's sample in the batch the producer state points at
+  auto fetch_idx = [&]() -> int {
+    const int b = pst[1] + lane;
+    return pst[0] < nsubs && lane < NB && b < pst[2] ? perm[b] : 0;
+  };
+  int pidx = 0;
+  auto produce_w = [&]() {  // the whole warp, converged
+    __syncwarp();
+    if (lane == 0) produce();
+    __syncwarp();
+    const int slot = pst[6];
+    if (lane < pst[5])
+      cp_async_cell<C>(reinterpret_cast<C*>(smem + slot * P::SB + P::W_BYTES + P::R_BYTES) + lane, funs + pidx);
+    cp_async_arrive_noinc(full + slot);
+    pidx = fetch_idx();
+  };
+  if constexpr (GATHER) {
+    pidx = fetch_idx();
+    for (int i = 0; i < S - 1; ++i) produce_w();
+  } else {
+    if (lane == 0)
+      for (int i = 0; i < S - 1; ++i) produce();
+  }
   __syncwarp();
 
   const int a = lane;
@@ -1879,7 +1909,7 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       const unsigned char* st = smem + slot * P::SB;
       const typename P::W* ws = reinterpret_cast<const typename P::W*>(st);
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
-      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + mt.foff;
+      const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (GATHER ? 0 : mt.foff);
       const int nb = (g.debug & 2) ? 0 : mt.nb;
       int jb = 0;
       int4 r = nb > 0 ? rs[0] : make_int4(0, 0, 0, 0);
@@ -1926,9 +1956,14 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
 #undef NFFTK_PIPE2_NODE
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(empty + slot);
-        produce();
+      if constexpr (GATHER) {
+        if (lane == 0) mbar_arrive(empty + slot);
+        produce_w();
+      } else {
+        if (lane == 0) {
+          mbar_arrive(empty + slot);
+          produce();
+        }
       }
       __syncwarp();
       if (mt.last) {
@@ -1975,6 +2010,13 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
 
 bool spread2_pipe_ok(const Geom& g) {
   return g.d == 2 && g.mode == MODE_TENSOR && g.psi && g.rec && pipe_geometry(g);
+}
+
+// Spreads that fetch their samples through perm themselves (no sorted copy,
+// no k_permute_samples): the residue spread and the d = 2 pipelined one.
+bool spread_gathers(const Geom& g, bool single) {
+  if (getenv("NFFTK_NO_GATHER")) return false;
+  return res_gathers(g, single) || spread2_pipe_ok(g);
 }
 
 bool spread_pipe_ok(const Geom& g, int elem_bytes) {
@@ -2080,8 +2122,8 @@ void launch_permute(bool single, const void* f, const int* perm, int64_t M, void
 }
 
 template <typename R, int D, int MM>
-static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const double* xs,
-                      const int*, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
+static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, const double* xs,
+                      const int* perm, const int4* subs, int nsubs, const Geom& g, cudaStream_t s) {
   if constexpr (D == 3 && MM > 0) {
     if constexpr (MM <= 6) {
       if (spread_pipe_ok(g, sizeof(cplx_t<R>))) {
@@ -2130,7 +2172,8 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
     if (spread2_pipe_ok(g)) {
       using P = Pipe2Cfg<R, MM, 8>;
       if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
-      auto kern = k_spread2_pipe<R, MM, 8>;
+      const bool gather = spread_gathers(g, sizeof(R) == 4);
+      auto kern = gather ? k_spread2_pipe<R, MM, 8, true> : k_spread2_pipe<R, MM, 8, false>;
       NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
       static int sms2 = 0;
       if (!sms2) {
@@ -2141,7 +2184,8 @@ static void spread_go(const CUtensorMap*, void* gp, const void*, void* fs, const
       int per_sm = 0;
       NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, P::SMEM));
       int grid = std::max(1, std::min(nsubs, sms2 * std::max(1, per_sm)));
-      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs, nsubs,
+      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, (const cplx_t<R>*)f,
+                                     gather ? perm : nullptr, g.psi, g.rec, subs, nsubs,
                                      sched_geom(g, nsubs, grid));
       count_launch();
       return;

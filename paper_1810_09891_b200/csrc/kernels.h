@@ -43,6 +43,7 @@ void build_recs(const double* xs, int64_t M, const Geom& g, int4* rec, unsigned*
 bool res_geometry(const Geom& g, bool single);
 bool res_ok(const Geom& g);
 bool res_gathers(const Geom& g, bool single);
+bool spread_gathers(const Geom& g, bool single);
 void launch_spread_res(bool single, void* grid, const void* fs, const void* f, const int* perm, const double* xs,
                        const int4* subs, int nsubs, const Geom& g, cudaStream_t s);
 

@@ -760,8 +760,8 @@ void plan_spread_device(Plan* p, const void* f, cudaStream_t s) {
   void* target = dense ? p->grid : p->gp;
   { PhaseScope ps(p, PH_ZERO, s);
     NFFTK_CUDA(cudaMemsetAsync(target, 0, dense ? p->elem_bytes() * (size_t)p->grid_size : p->gp_bytes, s)); }
-  // (the residue spread gathers the samples itself: no sorted copy)
-  if (!res_gathers(p->geom, p->single)) {
+  // (the residue spread and the d = 2 pipelined spread gather the samples themselves: no sorted copy)
+  if (!spread_gathers(p->geom, p->single)) {
     if (!p->f_sorted) NFFTK_CUDA(cudaMalloc(&p->f_sorted, p->elem_bytes() * (p->M + 2)));  // +2: aligned bulk copies
     PhaseScope ps(p, PH_PERMUTE, s); launch_permute(p->single, f, p->perm, p->M, p->f_sorted, s); }
   { PhaseScope ps(p, PH_SPREAD, s);

@@ -119,3 +119,24 @@ def test_dense_flush_matches_padded_fold(d, m, precision, oracle, monkeypatch):
     a, b = dense.adjoint(fs), padded.adjoint(fs)
     assert e2(b, a) < (1e-14 if precision == "double" else 1e-6)
     assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("m,M,kind", [(6, 4000, "edges"), (4, 17, "uniform"), (8, 5000, "dense")])
+def test_d2_sample_gather_matches_sorted_copy(m, M, kind, precision, oracle, monkeypatch):
+    """k_spread2_pipe fetches its samples through perm itself (one cp.async per
+    lane arriving on the batch's mbarrier); NFFTK_NO_GATHER reads the sorted
+    copy k_permute_samples makes.  Same adjoint, also on replays."""
+    N, n = (32, 32), (64, 64)
+    x = nodes(2, n, M, seed=40 + m, kind=kind)
+    rng = np.random.default_rng(6)
+    fs = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    monkeypatch.delenv("NFFTK_NO_GATHER", raising=False)
+    p = plan(N, n, m, x, precision, monkeypatch)
+    a = [p.adjoint(fs) for _ in range(3)]
+    monkeypatch.setenv("NFFTK_NO_GATHER", "1")
+    b = p.adjoint(fs)
+    monkeypatch.delenv("NFFTK_NO_GATHER")
+    assert e2(oracle.adjoint(N, n, m, x, fs), a[0]) < TOL[precision]
+    for v in a:
+        assert e2(b, v) < (1e-14 if precision == "double" else 1e-6)
