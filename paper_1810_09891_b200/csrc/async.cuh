@@ -41,6 +41,18 @@ __device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// cp.async of one cell with an L2 cache policy (createpolicy, e.g. evict-first
+// for data read once through a random index)
+template <typename C>
+__device__ __forceinline__ void cp_async_cell_hint(C* sdst, const C* gsrc, unsigned long long pol) {
+  if constexpr (sizeof(C) == 16)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+                 "l"(pol));
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+                 "l"(pol));
+}
+
 template <typename C>
 __device__ __forceinline__ void cp_async_cell(C* sdst, const C* gsrc) {
   if constexpr (sizeof(C) == 16) cp_async16(sdst, gsrc);

@@ -282,11 +282,13 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
         const int jj = j + qq * T;
         const int k = jj & (Ns - 1);
         const int ts = k * (L / (Ns * 4));
-#pragma unroll
-        for (int r = 1; r < 4; ++r) {
-          C w = tw[ts * r];
-          if (DIR > 0) w.y = -w.y;
-          x[4 * qq + r] = Cx<R>::mul(x[4 * qq + r], w);
+        {
+          C w1 = tw[ts];  // one load, w^2 and w^3 by products (as in the radix-8 stages)
+          if (DIR > 0) w1.y = -w1.y;
+          const C w2 = Cx<R>::mul(w1, w1), w3 = Cx<R>::mul(w1, w2);
+          x[4 * qq + 1] = Cx<R>::mul(x[4 * qq + 1], w1);
+          x[4 * qq + 2] = Cx<R>::mul(x[4 * qq + 2], w2);
+          x[4 * qq + 3] = Cx<R>::mul(x[4 * qq + 3], w3);
         }
         butterfly<R, DIR, 4>(x + 4 * qq);
         d0[qq] = (jj / Ns) * Ns * 4 + k;

@@ -237,6 +237,7 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
     return pst[0] < nsubs && b < pst[2] ? perm[b] : 0;
   };
   int pidx = 0;
+  const unsigned long long gpol = l2_evict_first_policy();
   // warp 0, converged: post the next batch; in gather mode every lane then
   // sends its sample after the batch's byte count is posted
   auto produce_w = [&]() {
@@ -246,8 +247,15 @@ k_spread_res(cplx_t<R>* __restrict__ grid, const cplx_t<R>* __restrict__ fsorted
       __syncwarp();
       const int slot = pst[7];
       if (lane < pst[6])
+#ifdef NFFTK_GATHER_NO_HINT
         cp_async_cell<C>(reinterpret_cast<C*>(smem + P::RING_OFF + slot * P::SB + P::W_BYTES + P::R_BYTES) + lane,
                          funs + pidx);
+#else
+        // read once through a random index: evict-first, so the 1 GiB sample
+        // array does not push the prefetched node rows out of L2
+        cp_async_cell_hint<C>(reinterpret_cast<C*>(smem + P::RING_OFF + slot * P::SB + P::W_BYTES + P::R_BYTES) + lane,
+                              funs + pidx, gpol);
+#endif
       cp_async_arrive_noinc(full + slot);
       pidx = fetch_idx();
     }
