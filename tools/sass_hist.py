@@ -13,9 +13,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_1810_09891_b200", "csrc", "build")
 KERNELS = [("residue.o", "k_spread_res"), ("gridding.o", "k_interp_pipe"), ("gridding.o", "k_spread_pipe"),
-           ("gridding.o", "k_spread2_pipe")]
+           ("gridding.o", "k_spread2_pipe"), ("fft.o", "k_fft_pass")]
 KEY = ("UTMALDG", "UTMAPF", "UBLKCP", "UBLKRED", "UBLKPF", "SYNCS", "DFMA", "DMUL", "FFMA", "LDS", "STS",
-       "SHFL", "ATOMS", "ATOMG", "RED", "BAR", "LDG", "STG")
+       "SHFL", "ATOMS", "ATOMG", "RED", "BAR", "LDG", "STG", "LDGSTS", "ARRIVES", "DADD")
 
 
 def main():
