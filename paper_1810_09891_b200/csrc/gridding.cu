@@ -1789,11 +1789,17 @@ struct Pipe2Cfg {
   static constexpr size_t SMEM = ROWS_OFF + al((size_t)H0 * HS * ELEM);
 };
 
-// GATHER: the samples are not read from a sorted copy but fetched by the
-// warp itself, lane l < NB bringing f[perm[base + l]] of the batch with one
+// GATHER: the samples are not read from a sorted copy but fetched by warp 0
+// itself, lane l < NB bringing f[perm[base + l]] of the batch with one
 // cp.async that arrives on the batch's mbarrier (as in residue.cu).
-template <typename R, int MM, int T1, bool GATHER>
-__global__ void __launch_bounds__(32)
+// NWARP warps share a tile: warp w takes nodes w, w + NWARP, ... of every
+// batch into its own register halo, and at the end of the tile the halos are
+// added up in the staging rows (lane a of every warp owns row a: no
+// conflicts) before one flush.  The ring and the staging rows -- the shared
+// memory that limited the one-warp CTAs to 8 warps per SM at C4 -- serve
+// NWARP warps; registers (84 accumulators per lane) stop it at two.
+template <typename R, int MM, int T1, bool GATHER, int NWARP>
+__global__ void __launch_bounds__(32 * NWARP)
 k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
                const cplx_t<R>* __restrict__ funs, const int* __restrict__ perm,
                const double* __restrict__ psi, const int4* __restrict__ rec,
@@ -1808,11 +1814,11 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
   StageMeta* meta = reinterpret_cast<StageMeta*>(empty + S);
   int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k, last batch: nodes, slot
   C* stage = reinterpret_cast<C*>(smem + P::ROWS_OFF);
-  const int lane = threadIdx.x;
-  if (lane == 0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(full + i, GATHER ? 33 : 1);
-      mbar_init(empty + i, 1);
+      mbar_init(empty + i, NWARP);
     }
     pst[0] = blockIdx.x;
     pst[4] = 0;
@@ -1823,7 +1829,8 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       pst[3] = sp.x;
     }
   }
-  __syncwarp();
+  if constexpr (NWARP > 1) __syncthreads();
+  else __syncwarp();
   auto produce = [&]() {
     const int pk = pst[4];
     const int slot = pk % S;
@@ -1884,12 +1891,14 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     cp_async_arrive_noinc(full + slot);
     pidx = fetch_idx();
   };
-  if constexpr (GATHER) {
-    pidx = fetch_idx();
-    for (int i = 0; i < S - 1; ++i) produce_w();
-  } else {
-    if (lane == 0)
-      for (int i = 0; i < S - 1; ++i) produce();
+  if (warp == 0) {
+    if constexpr (GATHER) {
+      pidx = fetch_idx();
+      for (int i = 0; i < S - 1; ++i) produce_w();
+    } else {
+      if (lane == 0)
+        for (int i = 0; i < S - 1; ++i) produce();
+    }
   }
   __syncwarp();
 
@@ -1911,8 +1920,8 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
       const int4* rs = reinterpret_cast<const int4*>(st + P::W_BYTES);
       const C* fv = reinterpret_cast<const C*>(st + P::W_BYTES + P::R_BYTES) + (GATHER ? 0 : mt.foff);
       const int nb = (g.debug & 2) ? 0 : mt.nb;
-      int jb = 0;
-      int4 r = nb > 0 ? rs[0] : make_int4(0, 0, 0, 0);
+      int jb = warp;  // this warp's nodes: warp, warp + NWARP, ...
+      int4 r = jb < nb ? rs[jb] : make_int4(0, 0, 0, 0);
       while (jb < nb) {
 #define NFFTK_PIPE2_NODE(H)                                                                \
   {                                                                                        \
@@ -1934,12 +1943,12 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     if constexpr (H + K <= H1) {                             \
       for (;;) {                                             \
         NFFTK_PIPE2_NODE(H)                                  \
-        if (++jb >= nb) break;                               \
+        if ((jb += NWARP) >= nb) break;                      \
         r = rs[jb];                                          \
         if (r.y != H) break;                                 \
       }                                                      \
     } else {                                                 \
-      if (++jb < nb) r = rs[jb];                             \
+      if ((jb += NWARP) < nb) r = rs[jb];                    \
     }                                                        \
     break;
         switch (r.y) {
@@ -1949,21 +1958,17 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
           NFFTK_PIPE2_CASE(12) NFFTK_PIPE2_CASE(13) NFFTK_PIPE2_CASE(14) NFFTK_PIPE2_CASE(15)
           NFFTK_PIPE2_CASE(16)
           default:
-            if (++jb < nb) r = rs[jb];
+            if ((jb += NWARP) < nb) r = rs[jb];
             break;
         }
 #undef NFFTK_PIPE2_CASE
 #undef NFFTK_PIPE2_NODE
       }
       __syncwarp();
-      if constexpr (GATHER) {
-        if (lane == 0) mbar_arrive(empty + slot);
-        produce_w();
-      } else {
-        if (lane == 0) {
-          mbar_arrive(empty + slot);
-          produce();
-        }
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (warp == 0) {
+        if constexpr (GATHER) produce_w();
+        else if (lane == 0) produce();
       }
       __syncwarp();
       if (mt.last) {
@@ -1973,35 +1978,55 @@ k_spread2_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted
     }
     if (tile < 0) break;  // end of work
     if (!(g.debug & 1)) {
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      // warp 0 stages its rows once the previous flush has read the staging
+      // area, the other warps add theirs, warp 0 sends the sums
       C* dst = stage + (size_t)a * HS;
+      if (warp == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < H1; ++c) {
-        C v;
-        v.x = accr[c];
-        v.y = acci[c];
-        dst[c] = v;
+        for (int c = 0; c < H1; ++c) {
+          C v;
+          v.x = accr[c];
+          v.y = acci[c];
+          dst[c] = v;
+        }
+        if constexpr (HS > H1) {
+          C z;
+          z.x = 0;
+          z.y = 0;
+          dst[H1] = z;
+        }
       }
-      if constexpr (HS > H1) {
-        C z;
-        z.x = 0;
-        z.y = 0;
-        dst[H1] = z;
+#pragma unroll
+      for (int w = 1; w < NWARP; ++w) {
+        __syncthreads();
+        if (warp == w) {
+#pragma unroll
+          for (int c = 0; c < H1; ++c) {
+            C v = dst[c];
+            v.x += accr[c];
+            v.y += acci[c];
+            dst[c] = v;
+          }
+        }
       }
-      fence_proxy_async_smem();
-      const int t0 = tile / g.ntile[1], t1 = tile - t0 * g.ntile[1];
-      bool done = false;
-      if (g.dense_flush) {
-        int ad = t0 * g.T[0] + a - g.m;
-        ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
-        bulk_red_row_wrapped<R>(gp, (int64_t)ad * g.n[1], t1 * T1 - g.m, g.n[1], dst, HS);
-        done = true;
+      if constexpr (NWARP > 1) __syncthreads();
+      if (warp == 0) {
+        fence_proxy_async_smem();
+        const int t0 = tile / g.ntile[1], t1 = tile - t0 * g.ntile[1];
+        bool done = false;
+        if (g.dense_flush) {
+          int ad = t0 * g.T[0] + a - g.m;
+          ad += ad < 0 ? g.n[0] : (ad >= g.n[0] ? -g.n[0] : 0);
+          bulk_red_row_wrapped<R>(gp, (int64_t)ad * g.n[1], t1 * T1 - g.m, g.n[1], dst, HS);
+          done = true;
+        }
+        if (!done) {
+          int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
+          bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
+        }
+        asm volatile("cp.async.bulk.commit_group;\n" ::);
       }
-      if (!done) {
-        int64_t row0 = (int64_t)(t0 * g.T[0] + a) * g.np[1] + t1 * T1;
-        bulk_red_add<R>(gp + row0, dst, (unsigned)(HS * sizeof(C)));
-      }
-      asm volatile("cp.async.bulk.commit_group;\n" ::);
     }
   }
   if (threadIdx.x == 0) sched_done(g, SCHED_SPREAD2);
@@ -2173,7 +2198,15 @@ static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, con
       using P = Pipe2Cfg<R, MM, 8>;
       if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
       const bool gather = spread_gathers(g, sizeof(R) == 4);
-      auto kern = gather ? k_spread2_pipe<R, MM, 8, true> : k_spread2_pipe<R, MM, 8, false>;
+      // complex128: two warps per tile (C4 spread 2.32 -> 2.00 ms: twice the
+      // warps on the same ring and staging rows); complex64 stays at one
+      // (1.36 ms with one, 1.37 with two, 1.70 with four).  NFFTK_SPREAD2_WARPS
+      // overrides for A/B runs and tests.
+      const char* we = getenv("NFFTK_SPREAD2_WARPS");
+      int nwarp = we ? atoi(we) : (sizeof(R) == 8 ? 2 : 1);
+      if (nwarp != 1 && nwarp != 2) nwarp = 2;
+      auto kern = gather ? k_spread2_pipe<R, MM, 8, true, 2> : k_spread2_pipe<R, MM, 8, false, 2>;
+      if (nwarp == 1) kern = gather ? k_spread2_pipe<R, MM, 8, true, 1> : k_spread2_pipe<R, MM, 8, false, 1>;
       NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
       static int sms2 = 0;
       if (!sms2) {
@@ -2182,9 +2215,9 @@ static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, con
         NFFTK_CUDA(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev));
       }
       int per_sm = 0;
-      NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, P::SMEM));
+      NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nwarp, P::SMEM));
       int grid = std::max(1, std::min(nsubs, sms2 * std::max(1, per_sm)));
-      kern<<<grid, 32, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, (const cplx_t<R>*)f,
+      kern<<<grid, 32 * nwarp, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, (const cplx_t<R>*)f,
                                      gather ? perm : nullptr, g.psi, g.rec, subs, nsubs,
                                      sched_geom(g, nsubs, grid));
       count_launch();

@@ -140,3 +140,22 @@ def test_d2_sample_gather_matches_sorted_copy(m, M, kind, precision, oracle, mon
     assert e2(oracle.adjoint(N, n, m, x, fs), a[0]) < TOL[precision]
     for v in a:
         assert e2(b, v) < (1e-14 if precision == "double" else 1e-6)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("warps", ["1", "2"])
+def test_d2_spread_warps_per_tile(warps, precision, oracle, monkeypatch):
+    """k_spread2_pipe with one or two warps per tile (the second takes every
+    other node of a batch; the register halos are added in the staging rows
+    before the flush): same adjoint, nodes on the periodic boundaries and in
+    one dense cell (several subproblems per tile)."""
+    monkeypatch.setenv("NFFTK_SPREAD2_WARPS", warps)
+    N, n, m = (32, 32), (64, 64), 6
+    for kind, M in (("edges", 5000), ("dense", 3000), ("uniform", 1)):
+        x = nodes(2, n, M, seed=50, kind=kind)
+        p = plan(N, n, m, x, precision, monkeypatch)
+        rng = np.random.default_rng(8)
+        fs = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+        ref = oracle.adjoint(N, n, m, x, fs)
+        for _ in range(2):
+            assert e2(ref, p.adjoint(fs)) < TOL[precision]
