@@ -188,7 +188,7 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
     const C* src = in + (int64_t)u * q.in_su + (int64_t)v * q.in_sv;
     const int se = (int)q.in_se;
     double fac = 1.0;
-    if (q.scale_in) fac = q.scale * q.col_u[u] * q.col_v[v];
+    if (q.scale_in) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * q.col_v[v];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       // band groups: q.in_off[r] is the compact index of element r T (the
@@ -313,7 +313,7 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
     C* dst = out + (int64_t)u * q.out_su + (int64_t)v * q.out_sv;
     const int se = (int)q.out_se;
     double fac = 1.0;
-    if (q.scale_out) fac = q.scale * q.col_u[u] * q.col_v[v];
+    if (q.scale_out) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * q.col_v[v];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       int k = q.out_off[NFFTK_EOFF(i) / T];
@@ -343,14 +343,15 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
         if (NFFTK_EOFF(i) + m + L < np2 && pc + L < np2) row[pc + L] = x[i];
       }
     };
-    put_row(out + ((int64_t)(u + m) * q.pad_np[1] + (v + m)) * np2);
+    const bool d3 = q.pad_d == 3;
+    put_row(out + ((d3 ? (int64_t)(u + m) * q.pad_np[1] : 0) + (v + m)) * np2);
     // image rows: slots within m (+2) of the edge of dims 0, 1
-    const bool ia = u + m >= q.pad_n[0] || u + m + q.pad_n[0] < q.pad_np[0];
+    const bool ia = d3 && (u + m >= q.pad_n[0] || u + m + q.pad_n[0] < q.pad_np[0]);
     const bool ib = v + m >= q.pad_n[1] || v + m + q.pad_n[1] < q.pad_np[1];
     if (ia || ib) {
-      for (int ka = -1; ka <= 1; ++ka) {
-        const int pa = u + m + ka * q.pad_n[0];
-        if (pa < 0 || pa >= q.pad_np[0]) continue;
+      for (int ka = d3 ? -1 : 0; ka <= (d3 ? 1 : 0); ++ka) {
+        const int pa = d3 ? u + m + ka * q.pad_n[0] : 0;
+        if (d3 && (pa < 0 || pa >= q.pad_np[0])) continue;
         for (int kb = -1; kb <= 1; ++kb) {
           const int pb = v + m + kb * q.pad_n[1];
           if (pb < 0 || pb >= q.pad_np[1] || (ka == 0 && kb == 0)) continue;
@@ -421,16 +422,16 @@ bool len_ok(int L) { return L == 64 || L == 128 || L == 256 || L == 512; }
 
 }  // namespace
 
-// d = 3, every n_i a supported power of two, N_i even and a multiple of the
-// CTA's line group where it is a line coordinate (N_2, and n_1 for the
-// contiguous pass).
+// d = 2 or 3, every n_i a supported power of two, N_i even; the band size
+// of the last dim (the line coordinate of the strided passes) a multiple of
+// the CTA's (half) line group.
 bool fft3_supported(int d, const int* n, const int* N, bool single) {
   if (getenv("NFFTK_NO_PRUNED_FFT")) return false;
-  if (d != 3) return false;
+  if (d != 3 && d != 2) return false;
   const int G = single ? 8 : 4;  // the half group of the strided passes
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < d; ++i)
     if (!len_ok(n[i]) || (N[i] & 1) || N[i] > n[i] || N[i] < 2) return false;
-  return N[2] % G == 0 && n[1] % G == 0;
+  return N[d - 1] % G == 0 && n[d - 2] % G == 0;
 }
 
 // exp(-2 pi i k / L), k = 0 .. L-1, rounded from long double
@@ -456,8 +457,52 @@ void fft3_twiddles(int L, bool single, std::vector<unsigned char>& out) {
 }
 
 size_t fft3_scratch_elems(const Fft3Geom& q) {
+  if (q.d == 2) return (size_t)q.n[0] * q.N[1];  // T (n0 x N1)
   // T1 (n0 x N1 x N2) followed by T2 (n0 x n1 x N2)
   return (size_t)q.n[0] * q.N[1] * q.N[2] + (size_t)q.n[0] * q.n[1] * q.N[2];
+}
+
+// d = 2: dim 0 on the N1 band columns (deconvolved on load) -> T[a][b'], then
+// dim 1 on all n0 rows into the (padded) grid; the adjoint in reverse.
+template <typename R>
+static void fft2_forward_t(const void* fhat, void* scratch, void* out, bool padded, const Fft3Geom& q,
+                           cudaStream_t s) {
+  const int64_t N1 = q.N[1], n1 = q.n[1];
+  FftPass b{};
+  b.nu = 1; b.nv = q.N[1];
+  b.in_su = 0; b.in_sv = 1; b.in_se = N1; b.in_band = q.N[0];
+  b.out_su = 0; b.out_sv = 1; b.out_se = N1; b.out_band = 0;
+  b.scale_in = 1; b.scale = 1.0 / q.grid_size; b.col_e = q.icol[0]; b.col_u = nullptr; b.col_v = q.icol[1];
+  b.pad_m = -1; b.tw = q.tw[0];
+  launch_pass<R>(fhat, scratch, b, q.n[0], -1, false, s);
+  FftPass c{};
+  c.nu = 1; c.nv = q.n[0];
+  c.in_su = 0; c.in_sv = N1; c.in_se = 1; c.in_band = q.N[1];
+  c.out_su = 0; c.out_sv = n1; c.out_se = 1; c.out_band = 0;
+  c.pad_m = padded ? q.m : -1; c.pad_d = 2;
+  c.pad_n[0] = 1; c.pad_np[0] = 1;
+  c.pad_n[1] = q.n[0]; c.pad_np[1] = q.np[0];
+  c.pad_n[2] = q.n[1]; c.pad_np[2] = q.np[1];
+  c.tw = q.tw[1];
+  launch_pass<R>(scratch, out, c, q.n[1], -1, true, s);
+}
+
+template <typename R>
+static void fft2_inverse_t(const void* grid, void* scratch_a, void* fhat, const Fft3Geom& q, cudaStream_t s) {
+  const int64_t N1 = q.N[1], n1 = q.n[1];
+  FftPass c{};  // dim 1: rows a of the dense grid -> T[a][b'] (band only)
+  c.nu = 1; c.nv = q.n[0];
+  c.in_su = 0; c.in_sv = n1; c.in_se = 1; c.in_band = 0;
+  c.out_su = 0; c.out_sv = N1; c.out_se = 1; c.out_band = q.N[1];
+  c.pad_m = -1; c.tw = q.tw[1];
+  launch_pass<R>(grid, scratch_a, c, q.n[1], 1, true, s);
+  FftPass b{};  // dim 0: band columns b' -> f_hat[a'][b'], deconvolved on store
+  b.nu = 1; b.nv = q.N[1];
+  b.in_su = 0; b.in_sv = 1; b.in_se = N1; b.in_band = 0;
+  b.out_su = 0; b.out_sv = 1; b.out_se = N1; b.out_band = q.N[0];
+  b.scale_out = 1; b.scale = 1.0 / q.grid_size; b.col_e = q.icol[0]; b.col_u = nullptr; b.col_v = q.icol[1];
+  b.pad_m = -1; b.tw = q.tw[0];
+  launch_pass<R>(scratch_a, fhat, b, q.n[0], 1, false, s);
 }
 
 template <typename R>
@@ -484,7 +529,7 @@ static void fft3_forward_t(const void* fhat, void* scratch, void* out, bool padd
   c.nu = q.n[0]; c.nv = q.n[1];
   c.in_su = n1 * N2; c.in_sv = N2; c.in_se = 1; c.in_band = q.N[2];
   c.out_su = n1 * n2; c.out_sv = n2; c.out_se = 1; c.out_band = 0;
-  c.pad_m = padded ? q.m : -1;
+  c.pad_m = padded ? q.m : -1; c.pad_d = 3;
   for (int i = 0; i < 3; ++i) { c.pad_n[i] = q.n[i]; c.pad_np[i] = q.np[i]; }
   c.tw = q.tw[2];
   launch_pass<R>(t2, out, c, q.n[2], -1, true, s);
@@ -520,12 +565,22 @@ static void fft3_inverse_t(const void* grid, void* scratch_a, void* scratch_b, v
 
 void fft3_forward(bool single, const void* fhat, void* scratch, void* out, bool padded, const Fft3Geom& q,
                   cudaStream_t s) {
+  if (q.d == 2) {
+    if (single) fft2_forward_t<float>(fhat, scratch, out, padded, q, s);
+    else fft2_forward_t<double>(fhat, scratch, out, padded, q, s);
+    return;
+  }
   if (single) fft3_forward_t<float>(fhat, scratch, out, padded, q, s);
   else fft3_forward_t<double>(fhat, scratch, out, padded, q, s);
 }
 
 void fft3_inverse(bool single, const void* grid, void* scratch_a, void* scratch_b, void* fhat,
                   const Fft3Geom& q, cudaStream_t s) {
+  if (q.d == 2) {
+    if (single) fft2_inverse_t<float>(grid, scratch_a, fhat, q, s);
+    else fft2_inverse_t<double>(grid, scratch_a, fhat, q, s);
+    return;
+  }
   if (single) fft3_inverse_t<float>(grid, scratch_a, scratch_b, fhat, q, s);
   else fft3_inverse_t<double>(grid, scratch_a, scratch_b, fhat, q, s);
 }

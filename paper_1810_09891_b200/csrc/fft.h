@@ -1,4 +1,4 @@
-// Pruned three-pass FFT of the oversampled grid for d = 3 plans (fft.cu).
+// Pruned FFT of the oversampled grid for d = 3 (three passes) and d = 2 (two passes) plans (fft.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,11 +27,13 @@ struct FftPass {
   const double* col_u;
   const double* col_v;
   int pad_m;                         // >= 0: store into the ghost-padded grid (u, v = slots of dims 0, 1)
+  int pad_d;                         // 3: (u, v, line); 2: (v, line) with pad_n / pad_np at [1], [2]
   int pad_n[3], pad_np[3];
   const void* tw;                    // exp(-2 pi i k / L), k < L, in the pass's precision
 };
 
 struct Fft3Geom {
+  int d;                             // 3, or 2 (dims at [0], [1])
   int N[3], n[3], np[3];
   int m;
   const double* icol[3];             // device: 1 / (phi_hat_i(k) wscale_i) over k + N_i/2

@@ -572,9 +572,10 @@ static void ensure_grid(Plan* p) {
   if (!p->tmap_ready) build_tensor_map(p);
   // pruned F / F^H (fft.cu) where the geometry allows it and its two
   // intermediate arrays fit the dense grid buffer (the trafo's scratch)
-  p->fft3 = p->d == 3 && fft3_supported(p->d, p->n.data(), p->N.data(), p->single);
+  p->fft3 = p->d <= MAX_D && fft3_supported(p->d, p->n.data(), p->N.data(), p->single);
   if (p->fft3) {
-    for (int i = 0; i < 3; ++i) {
+    p->fq.d = p->d;
+    for (int i = 0; i < p->d; ++i) {
       p->fq.N[i] = p->N[i];
       p->fq.n[i] = p->n[i];
       p->fq.np[i] = p->geom.np[i];
@@ -584,7 +585,7 @@ static void ensure_grid(Plan* p) {
   if (p->fft3) {
     p->fq.m = p->m;
     p->fq.grid_size = (double)p->grid_size;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < p->d; ++i) {
       if (!p->fft_tw[i]) {
         std::vector<unsigned char> tw;
         fft3_twiddles(p->n[i], p->single, tw);

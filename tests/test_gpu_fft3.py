@@ -26,7 +26,7 @@ def e2(ref, got):
 
 def run(N, n, m, M, precision, seed=3):
     rng = np.random.default_rng(seed)
-    x = rng.random((M, 3)) - 0.5
+    x = rng.random((M, len(N))) - 0.5
     x[0] = -0.5  # halo wrap in every dim: reads the ghost layers the last pass writes
     x[1] = np.nextafter(0.5, 0.0)
     K = int(np.prod(N))
@@ -111,3 +111,32 @@ def test_repeated_and_chained_transforms(oracle):
         assert e2(a_ref, p.adjoint(fs)) < 1e-12
         assert e2(f_ref, p.trafo(fh)) < 1e-12
     p.close()
+
+
+CASES_2D = [
+    ((256, 256), (512, 512), 8),     # C2
+    ((32, 64), (64, 256), 4),
+    ((128, 16), (256, 64), 6),
+    ((40, 24), (64, 64), 3),         # sigma < 2
+    ((2, 8), (64, 128), 2),
+]
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("N,n,m", CASES_2D)
+def test_pruned_fft_d2_matches_oracle(N, n, m, precision, oracle):
+    """d = 2: two passes (dim 0 on the band columns, dim 1 on all rows into
+    the padded grid; the adjoint in reverse)."""
+    M = 3000
+    x, fh, fs, (path, f, a) = run(N, n, m, M, precision)
+    assert path == "pruned"
+    assert e2(oracle.trafo(N, n, m, x, fh), f) < TOL[precision]
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
+
+
+def test_pruned_fft_d2_long_lines_take_cufft(oracle):
+    N, n, m = (512, 64), (1024, 128), 4
+    x, fh, fs, (path, f, a) = run(N, n, m, 2000, "double")
+    assert path == "cufft"
+    assert e2(oracle.trafo(N, n, m, x, fh), f) < 1e-12
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < 1e-12
