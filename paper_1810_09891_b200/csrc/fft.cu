@@ -381,12 +381,27 @@ int strided_group() {
   return half ? FftCfg<R>::W / 2 : FftCfg<R>::W;
 }
 
+// Long lines (L >= 1024): the CTA holds at most 1024 threads and ~128 KB of
+// lines, so the strided groups shrink to 1024 / (L / 8) lines (8 at 1024, 4
+// at 2048, 2 at 4096: 128- to 32-byte global segments) on the skewed layout,
+// and the contiguous pass takes one or two lines per CTA.
+template <typename R, int L>
+constexpr int fft_strided_full() {
+  return FftCfg<R>::W * (L / 8) <= 1024 ? FftCfg<R>::W : 1024 / (L / 8);
+}
+template <typename R, int L>
+constexpr int fft_contig_group() {
+  return FftCfg<R>::GE * (L / 8) <= 512 ? FftCfg<R>::GE : (512 / (L / 8) > 0 ? 512 / (L / 8) : 1);
+}
+
 template <typename R, int L, int DIR>
 void launch_pass_d(const void* in, void* out, const FftPass& q, bool ef, cudaStream_t s) {
-  constexpr int W = FftCfg<R>::W;
-  if (ef) launch_pass_t<R, L, DIR, true, FftCfg<R>::GE>(in, out, q, s);
-  else if (q.nv % W == 0 && strided_group<R>() == W) launch_pass_t<R, L, DIR, false, W>(in, out, q, s);
-  else launch_pass_t<R, L, DIR, false, W / 2>(in, out, q, s);
+  constexpr int GF = fft_strided_full<R, L>();
+  constexpr int GH = GF > 2 ? GF / 2 : GF;
+  if (ef) launch_pass_t<R, L, DIR, true, fft_contig_group<R, L>()>(in, out, q, s);
+  else if (q.nv % GF == 0 && (GH == GF || strided_group<R>() == FftCfg<R>::W))
+    launch_pass_t<R, L, DIR, false, GF>(in, out, q, s);
+  else launch_pass_t<R, L, DIR, false, GH>(in, out, q, s);
 }
 
 template <typename R, int L>
@@ -414,11 +429,14 @@ void launch_pass(const void* in, void* out, const FftPass& q0, int L, int dir, b
     case 128: launch_pass_l<R, 128>(in, out, q, dir, ef, s); break;
     case 256: launch_pass_l<R, 256>(in, out, q, dir, ef, s); break;
     case 512: launch_pass_l<R, 512>(in, out, q, dir, ef, s); break;
+    case 1024: launch_pass_l<R, 1024>(in, out, q, dir, ef, s); break;
+    case 2048: launch_pass_l<R, 2048>(in, out, q, dir, ef, s); break;
+    case 4096: launch_pass_l<R, 4096>(in, out, q, dir, ef, s); break;
     default: fail(EK_CUDA, "pruned FFT: unsupported line length " + std::to_string(L));
   }
 }
 
-bool len_ok(int L) { return L == 64 || L == 128 || L == 256 || L == 512; }
+bool len_ok(int L) { return L >= 64 && L <= 4096 && (L & (L - 1)) == 0; }
 
 }  // namespace
 

@@ -134,8 +134,31 @@ def test_pruned_fft_d2_matches_oracle(N, n, m, precision, oracle):
     assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
 
 
-def test_pruned_fft_d2_long_lines_take_cufft(oracle):
-    N, n, m = (512, 64), (1024, 128), 4
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("N,n", [((512, 32), (1024, 64)), ((32, 512), (64, 1024)), ((1024, 16), (2048, 64)),
+                                 ((16, 1024), (64, 2048)), ((2048, 8), (4096, 64)), ((8, 2048), (64, 4096)),
+                                 ((1000, 24), (2048, 64))])
+def test_pruned_fft_d2_long_lines(N, n, precision, oracle):
+    """Lines of 1024..4096 (four radix stages; strided groups of 8 / 4 / 2
+    lines on the skewed layout, one or two lines per CTA in the contiguous
+    pass), as dim 0 and as dim 1."""
+    m, M = 4, 3000
+    x, fh, fs, (path, f, a) = run(N, n, m, M, precision)
+    assert path == "pruned"
+    assert e2(oracle.trafo(N, n, m, x, fh), f) < TOL[precision]
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
+
+
+def test_pruned_fft_d3_long_line(oracle):
+    N, n, m, M = (16, 512, 8), (64, 1024, 64), 3, 2000
+    x, fh, fs, (path, f, a) = run(N, n, m, M, "double")
+    assert path == "pruned"
+    assert e2(oracle.trafo(N, n, m, x, fh), f) < 1e-12
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < 1e-12
+
+
+def test_pruned_fft_d2_longer_lines_take_cufft(oracle):
+    N, n, m = (4096, 16), (8192, 64), 4
     x, fh, fs, (path, f, a) = run(N, n, m, 2000, "double")
     assert path == "cufft"
     assert e2(oracle.trafo(N, n, m, x, fh), f) < 1e-12
