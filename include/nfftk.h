@@ -164,7 +164,7 @@ int32_t nfftk_deconv_cols(int32_t handle, int32_t dim, double * out, int64_t len
  * ready, factor mode, tiles, subproblems, sum of stencil widths, gridding
  * kernels (0 batch, 1 pipelined row-per-thread, 2 residue-owned spread),
  * nodes with a 2m+1 wide stencil (residue geometry), F / F^H (0 cuFFT on the
- * dense grid, 1 pruned three-pass line FFTs with D, D^H and the ghost padding
+ * dense grid, 1 pruned two-/three-pass line FFTs with D, D^H and the ghost padding
  * fused in); count <= 16 */
 int32_t nfftk_get_params(int32_t handle, int64_t * out, int32_t count);
 int32_t nfftk_get_sizes(int32_t handle, int32_t * N, int32_t * n, int32_t * tile, int32_t count);

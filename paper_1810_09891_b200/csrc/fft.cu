@@ -1,6 +1,6 @@
-// Pruned oversampled FFT for d = 3 plans (sm_100a): F and F^H as three passes
-// of hand-written 1-D line FFTs, with D / D^H and the ghost-padded layout
-// fused into the first and last pass.
+// Pruned oversampled FFT for d = 3 and d = 2 plans (sm_100a): F and F^H as
+// three (two) passes of hand-written 1-D line FFTs, with D / D^H and the
+// ghost-padded layout fused into the first and last pass.
 //
 //   trafo   g = F (D f_hat)        transform.py:96-104  (deconvolve, zero-pad, fft_nd sign -1)
 //   adjoint f_hat = D^H (F^H g)    transform.py:170-176 (fft_nd sign +1, pack, deconvolve)
@@ -21,8 +21,11 @@
 // position and at its periodic images, so the gather's halo is one TMA box)
 // and the last store of the adjoint (band only, scaled).
 //
+// (d = 2: dim 0 on the N1 band columns, then dim 1 on all n0 rows.)
+//
 // One line = Stockham autosort, radix 8 (then 4), L / 8 threads with 8
-// complex registers each, stages exchanged through shared memory.  Strided
+// complex registers each, stages exchanged through shared memory; L = 64 ..
+// 4096.  Strided
 // passes (dims 0, 1) give a CTA G adjacent lines (adjacent last-dim cells):
 // lanes run across the lines, so global accesses are 128-byte segments and
 // the shared-memory layout [element][line] is conflict-free for any stage.
