@@ -364,6 +364,8 @@ def main():
     roof = roofline(w, phases, args.steps, s_elem, peaks, fp64 if s_elem == 16 else fp32,
                     tuple(plan.tile), args.psi, sm_mhz=clk.get("sm_mhz") or clk.get("sm_max_mhz"),
                     gridding=plan.gridding)
+    if roof is not None and plan.fft == "pruned":
+        roof["other"].update(fft_roofline(w, phases, s_elem, peaks, plan))
 
     if rank != 0:
         if world > 1:
@@ -547,6 +549,37 @@ def smem_roof(w, s, per_ms, sm_mhz):
     return {"achieved": achieved, "peak": peak, "unit": "TB/s", "frac": achieved / peak,
             "algorithmic_bytes_per_launch": alg,
             "peak_source": f"{sms} SMs x 128 B/clk x {sm_mhz:.0f} MHz (sampled SM clock)"}
+
+
+def fft_roofline(w, phases, s, peaks, plan):
+    """The pruned F / F^H passes (csrc/fft.cu: k_fft_pass, with D, D^H and the
+    ghost padding fused in) against measured HBM.  Algorithmic bytes: every
+    pass reads its input and writes its output once -- f_hat, the band-compact
+    intermediates (n0 N1 N2 and n0 n1 N2 cells for d = 3, n0 N1 for d = 2) and
+    the ghost-padded grid (trafo) or the dense grid (adjoint)."""
+    import numpy as np
+
+    n, N = w.n, w.N
+    inter = []
+    for k in range(1, w.d):  # after pass k the first k dims are full, the rest band
+        inter.append(int(np.prod(n[:k])) * int(np.prod(N[k:])))
+    npad = 1
+    for i in range(w.d):
+        ntile = -(-n[i] // plan.tile[i])
+        npad *= ntile * plan.tile[i] + 2 * w.m + 2
+    cells = {"fft_fwd": w.num_freqs + 2 * sum(inter) + npad, "fft_inv": w.grid_size + 2 * sum(inter) + w.num_freqs}
+    out = {}
+    for ph, c in cells.items():
+        ms, calls = phases.get(ph, (0.0, 0))
+        if not calls:
+            continue
+        per = ms / calls
+        achieved = c * s / (per * 1e-3) / 1e9
+        out[ph] = {"kernel": "k_fft_pass (%d passes incl. %s)" % (w.d, "D + ghost padding" if ph == "fft_fwd" else "pack + D^H"),
+                   "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                   "frac": achieved / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": c * s,
+                   "avg_launch_ms": per, "peak_source": peaks["source"]}
+    return out
 
 
 def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None, sm_mhz=None, gridding=None):
