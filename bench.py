@@ -609,6 +609,16 @@ def roofline(w, phases, steps, s, peaks, fma_tflops, tile, psi=None, sm_mhz=None
                     "flops_per_launch": flops,
                     "peak_source": "k_fma_peak microbenchmark (measured in run)"},
         }
+        if psi in (None, "flags", "tensor"):
+            # PRE_PSI mode (the reference's default f1) streams the factor table
+            # M x d x (2m+1) doubles (kernels.py:56-72) every transform: with
+            # it the compulsory bytes are what the DRAM traffic compares with
+            alg_psi = traffic_alg + 8 * w.d * (2 * w.m + 1) * w.M
+            out[ph]["hbm_with_pre_psi_table"] = {
+                "algorithmic_bytes_per_launch": alg_psi,
+                "achieved": alg_psi / (per * 1e-3) / 1e9, "unit": "GB/s",
+                "frac": alg_psi / (per * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                "traffic_over_algorithmic": (out[ph]["traffic"] / alg_psi) if out[ph]["traffic"] else None}
         if ph == "interp":
             out[ph]["smem"] = smem_roof(w, s, per, sm_mhz)
     if not out:
