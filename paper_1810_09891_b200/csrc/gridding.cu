@@ -1292,9 +1292,13 @@ struct PipeCfg {
   static constexpr size_t SMEM = ROWS_OFF + rows_bytes;
 };
 
-template <typename R, int MM>
+// GATHER: warp 0 fetches the batch's samples through perm itself (lane l <
+// NB: one cp.async of f[perm[base + l]] arriving on the batch's mbarrier, the
+// index loaded one batch ahead) instead of reading a sorted copy (residue.cu).
+template <typename R, int MM, bool GATHER>
 __global__ void __launch_bounds__(PipeCfg<R, MM>::THREADS, PipeCfg<R, MM>::BLOCKS)
 k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
+              const cplx_t<R>* __restrict__ funs, const int* __restrict__ perm,
               const double* __restrict__ psi, const int4* __restrict__ rec,
               const int4* __restrict__ subs, int nsubs, Geom g) {
   using C = cplx_t<R>;
@@ -1324,12 +1328,13 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + P::CTL);
   unsigned long long* empty = full + S;
   StageMeta* meta = reinterpret_cast<StageMeta*>(empty + S);
-  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k
+  int* pst = reinterpret_cast<int*>(meta + S);  // producer: s, base, end, tile, k, last batch: nodes, slot
   C* stage = reinterpret_cast<C*>(smem + P::ROWS_OFF);  // per-thread staging rows
   const int lane = threadIdx.x & 31;
+  static_assert(NB <= 32, "gather: one sample per lane of warp 0");
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(full + i, 1);
+      mbar_init(full + i, GATHER ? 33 : 1);
       mbar_init(empty + i, NW);
     }
     pst[0] = blockIdx.x;
@@ -1351,6 +1356,10 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     if (pk >= S) mbar_wait(empty + slot, ((pk / S) - 1) & 1);
     StageMeta* mt = meta + slot;
     pst[4] = pk + 1;
+    if (GATHER) {
+      pst[5] = 0;
+      pst[6] = slot;
+    }
     if (pst[0] >= nsubs) {
       mt->nb = -1;
       mbar_arrive(full + slot);
@@ -1358,7 +1367,7 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     }
     const int pbase = pst[1], pend = pst[2];
     const int nb = min(NB, pend - pbase);
-    const int foff = pbase & (FA - 1);
+    const int foff = GATHER ? 0 : pbase & (FA - 1);
     const int fcnt = (nb + foff + FA - 1) & ~(FA - 1);
     mt->tile = pst[3];
     mt->nb = nb;
@@ -1366,11 +1375,12 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
     mt->foff = foff;
     unsigned char* st = smem + slot * P::SB;
     const unsigned wb = (unsigned)(sizeof(typename P::W) * PR) * nb, rb = 16u * nb,
-                   fb = (unsigned)sizeof(C) * fcnt;
+                   fb = GATHER ? 0u : (unsigned)sizeof(C) * fcnt;
     mbar_expect_tx(full + slot, wb + rb + fb);
+    if (GATHER) pst[5] = nb;
     bulk_g2s(st, reinterpret_cast<const typename P::W*>(psi) + (int64_t)pbase * PR, wb, full + slot);
     bulk_g2s(st + P::W_BYTES, rec + pbase, rb, full + slot);
-    bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
+    if (!GATHER) bulk_g2s(st + P::W_BYTES + P::R_BYTES, fsorted + (pbase - foff), fb, full + slot);
     if (pbase + nb < pend) {
       pst[1] = pbase + nb;
     } else {
@@ -1384,8 +1394,32 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }
     }
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < S - 1; ++i) produce();
+  auto fetch_idx = [&]() -> int {  // warp 0: this lane's sample index in the batch the producer points at
+    const int b = pst[1] + lane;
+    return pst[0] < nsubs && lane < NB && b < pst[2] ? perm[b] : 0;
+  };
+  int pidx = 0;
+  const unsigned long long gpol = l2_evict_first_policy();
+  auto produce_w = [&]() {  // warp 0, converged
+    __syncwarp();
+    if (lane == 0) produce();
+    __syncwarp();
+    const int slot = pst[6];
+    if (lane < pst[5])
+      cp_async_cell_hint<C>(reinterpret_cast<C*>(smem + slot * P::SB + P::W_BYTES + P::R_BYTES) + lane, funs + pidx,
+                            gpol);
+    cp_async_arrive_noinc(full + slot);
+    pidx = fetch_idx();
+  };
+  if constexpr (GATHER) {
+    if (threadIdx.x < 32) {
+      pidx = fetch_idx();
+      for (int i = 0; i < S - 1; ++i) produce_w();
+    }
+  } else {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < S - 1; ++i) produce();
+  }
 
   // contiguous row ownership: a warp holds ~1.5 halo a-lines and skips
   // (warp-uniformly) the nodes whose stencil misses them -- measured 12%
@@ -1558,7 +1592,11 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
-      if (threadIdx.x == 0) produce();
+      if constexpr (GATHER) {
+        if (threadIdx.x < 32) produce_w();
+      } else {
+        if (threadIdx.x == 0) produce();
+      }
       if (mt.last) {
         ++k;
         break;
@@ -1710,7 +1748,11 @@ k_spread_pipe(cplx_t<R>* __restrict__ gp, const cplx_t<R>* __restrict__ fsorted,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
-      if (threadIdx.x == 0) produce();
+      if constexpr (GATHER) {
+        if (threadIdx.x < 32) produce_w();
+      } else {
+        if (threadIdx.x == 0) produce();
+      }
       if (mt.last) {
         ++k;
         break;
@@ -2038,10 +2080,12 @@ bool spread2_pipe_ok(const Geom& g) {
 }
 
 // Spreads that fetch their samples through perm themselves (no sorted copy,
-// no k_permute_samples): the residue spread and the d = 2 pipelined one.
+// no k_permute_samples): the residue spread and the pipelined d = 2 / d = 3 ones.
+bool spread_pipe_ok(const Geom& g, int elem_bytes);
 bool spread_gathers(const Geom& g, bool single) {
   if (getenv("NFFTK_NO_GATHER")) return false;
-  return res_gathers(g, single) || spread2_pipe_ok(g);
+  if (res_ok(g)) return res_gathers(g, single);
+  return spread2_pipe_ok(g) || (g.d == 3 && g.m <= 6 && spread_pipe_ok(g, single ? 8 : 16));
 }
 
 bool spread_pipe_ok(const Geom& g, int elem_bytes) {
@@ -2156,7 +2200,8 @@ static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, con
         static_assert(P::NB > 0 && P::S >= 2, "pipe ring does not fit");
         if (g.HS != P::HS) fail(EK_CUDA, "pipe spread: halo row stride mismatch");
         if (g.psi_pad != (P::STEN3 ? 2 : 1)) fail(EK_CUDA, "pipe spread: PRE_PSI layout mismatch");
-        auto kern = k_spread_pipe<R, MM>;
+        const bool gather = spread_gathers(g, sizeof(R) == 4);
+        auto kern = gather ? k_spread_pipe<R, MM, true> : k_spread_pipe<R, MM, false>;
         NFFTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
         static int sms = 0;
         if (!sms) {
@@ -2167,8 +2212,9 @@ static void spread_go(const CUtensorMap*, void* gp, const void* f, void* fs, con
         int per_sm = 0;
         NFFTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::THREADS, P::SMEM));
         int grid = std::max(1, std::min(nsubs, sms * std::max(1, per_sm)));
-        kern<<<grid, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, g.psi, g.rec, subs,
-                                               nsubs, sched_geom(g, nsubs, grid));
+        kern<<<grid, P::THREADS, P::SMEM, s>>>((cplx_t<R>*)gp, (const cplx_t<R>*)fs, (const cplx_t<R>*)f,
+                                               gather ? perm : nullptr, g.psi, g.rec, subs, nsubs,
+                                               sched_geom(g, nsubs, grid));
         count_launch();
         return;
       }
