@@ -147,7 +147,7 @@ template <typename R, int D, int MM, int TEAM, typename W>
 __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, int HS, int H1, int K,
                                             const int* q, const W* w0, const W* w1,
                                             const W* wl, int o0, int o1, int tl, R& are,
-                                            R& aim) {
+                                            R& aim, int sh = 0) {
   using C = cplx_t<R>;
   if (MM > 0 && q[2 * D]) {
     constexpr int WF = 2 * (MM > 0 ? MM : 1);
@@ -225,7 +225,42 @@ __device__ __forceinline__ void interp_node(const cplx_t<R>* __restrict__ halo, 
 #pragma unroll
       for (int t = 0; t < WF; ++t) w2r[t] = (R)wl[t];
       const C* corner = halo + (q[0] * H1 + q[1]) * HS + q[2];
-      if constexpr (TEAM == WF) {
+      if constexpr (TEAM == WF && sizeof(R) == 4) {
+        // complex64, 8-lane teams: a half warp (one 8-byte shared-memory
+        // wavefront) holds two teams, whose rows start an even number of
+        // 4-byte words apart -- they collide in the banks whenever the two
+        // nodes' last-dim starts have the same parity (half of the time: 1.5
+        // wavefronts per load, ncu: 32% of the gather's wavefronts were
+        // conflicts).  sh = 1 tells the odd team of such a pair to walk its
+        // rows rotated by one cell (cells 1..7, then 0): the two footprints
+        // interleave and every load is one wavefront.
+        const R f1 = (R)w1[o1 + tl];
+        R wa[WF - 1];
+#pragma unroll
+        for (int t = 0; t < WF - 1; ++t) wa[t] = sh ? w2r[t + 1] : w2r[t];
+        const R wlast = sh ? w2r[0] : w2r[WF - 1];
+        const int dl = sh ? 0 : WF - 1;
+        const C* row = corner + tl * HS;
+#pragma unroll 2
+        for (int t0 = 0; t0 < WF; ++t0, row += H1 * HS) {
+          const C* p1 = row + sh;
+          R sre = 0, sim = 0;
+#pragma unroll
+          for (int t = 0; t < WF - 1; ++t) {
+            C v = p1[t];
+            sre = fma(wa[t], v.x, sre);
+            sim = fma(wa[t], v.y, sim);
+          }
+          {
+            C v = row[dl];
+            sre = fma(wlast, v.x, sre);
+            sim = fma(wlast, v.y, sim);
+          }
+          R w01 = (R)(w0[o0 + t0] * f1);
+          are = fma(w01, sre, are);
+          aim = fma(w01, sim, aim);
+        }
+      } else if constexpr (TEAM == WF) {
         // lane tl walks the WF rows (t0, tl), t0 = 0 .. WF-1: its dim-1
         // factor is fixed and the row pointer advances by one halo plane --
         // no per-row index arithmetic, one factor load less per row
@@ -766,6 +801,16 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
           q[4] = (wp >> 24) & 1;
         }
         R are = 0, aim = 0;
+        // complex64 8-lane teams (interp_node): the odd team of a half warp
+        // walks its rows rotated when the pair's last-dim starts share parity
+        int sh = 0;
+        if constexpr (D == 3 && sizeof(R) == 4 && TEAM == 8 && !P::HALF) {
+          const int q2p = __shfl_xor_sync(0xffffffffu, q[2], 8);
+          sh = ((lane >> 3) & 1) & ~((q[2] ^ q2p) & 1) & (int)q[6];
+#ifdef NFFTK_NO_ROT
+          sh = 0;
+#endif
+        }
         if (active) {
           const typename P::W* w = ws + jj * PR;
           // factor blocks: leading dims at w + OW0 / OW1 (indexed from the
@@ -788,7 +833,7 @@ k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ 
                                           tl, are, aim);
           } else if constexpr (D == 3)
             interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w + P::OW0, w + P::OW1, w + P::OWL, o0, o1,
-                                        tl, are, aim);
+                                        tl, are, aim, sh);
           else  // stencil-indexed rows [2m+1 | 2m+1]
             interp_node<R, D, MM, TEAM>(halo, HS, H1, K, q, w, w, w + K, 0, 0, tl, are, aim);
         }
