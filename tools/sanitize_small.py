@@ -1,4 +1,5 @@
-"""Small plans through every new kernel path, for compute-sanitizer runs:
+"""Small plans through every new kernel path (adjoint-identity sanity check; also the
+driver for compute-sanitizer where the pool allows it):
    compute-sanitizer --tool memcheck|racecheck python tools/sanitize_small.py
 (pruned FFT d=2 / d=3 incl. long lines and both line groups, gathering spreads:
 residue, d=2 one / two warps, d=3 rows; complex128 and complex64)."""
