@@ -191,7 +191,7 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
     const C* src = in + (int64_t)u * q.in_su + (int64_t)v * q.in_sv;
     const int se = (int)q.in_se;
     double fac = 1.0;
-    if (q.scale_in) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * q.col_v[v];
+    if (q.scale_in) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * (q.col_v ? q.col_v[v] : 1.0);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       // band groups: q.in_off[r] is the compact index of element r T (the
@@ -316,7 +316,7 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
     C* dst = out + (int64_t)u * q.out_su + (int64_t)v * q.out_sv;
     const int se = (int)q.out_se;
     double fac = 1.0;
-    if (q.scale_out) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * q.col_v[v];
+    if (q.scale_out) fac = q.scale * (q.col_u ? q.col_u[u] : 1.0) * (q.col_v ? q.col_v[v] : 1.0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       int k = q.out_off[NFFTK_EOFF(i) / T];
@@ -346,11 +346,11 @@ k_fft_pass(const cplx_t<R>* __restrict__ in, cplx_t<R>* __restrict__ out, FftPas
         if (NFFTK_EOFF(i) + m + L < np2 && pc + L < np2) row[pc + L] = x[i];
       }
     };
-    const bool d3 = q.pad_d == 3;
-    put_row(out + ((d3 ? (int64_t)(u + m) * q.pad_np[1] : 0) + (v + m)) * np2);
+    const bool d3 = q.pad_d == 3, d1 = q.pad_d == 1;
+    put_row(d1 ? out : out + ((d3 ? (int64_t)(u + m) * q.pad_np[1] : 0) + (v + m)) * np2);
     // image rows: slots within m (+2) of the edge of dims 0, 1
     const bool ia = d3 && (u + m >= q.pad_n[0] || u + m + q.pad_n[0] < q.pad_np[0]);
-    const bool ib = v + m >= q.pad_n[1] || v + m + q.pad_n[1] < q.pad_np[1];
+    const bool ib = !d1 && (v + m >= q.pad_n[1] || v + m + q.pad_n[1] < q.pad_np[1]);
     if (ia || ib) {
       for (int ka = d3 ? -1 : 0; ka <= (d3 ? 1 : 0); ++ka) {
         const int pa = d3 ? u + m + ka * q.pad_n[0] : 0;
@@ -401,7 +401,8 @@ template <typename R, int L, int DIR>
 void launch_pass_d(const void* in, void* out, const FftPass& q, bool ef, cudaStream_t s) {
   constexpr int GF = fft_strided_full<R, L>();
   constexpr int GH = GF > 2 ? GF / 2 : GF;
-  if (ef) launch_pass_t<R, L, DIR, true, fft_contig_group<R, L>()>(in, out, q, s);
+  if (ef && q.nv % fft_contig_group<R, L>() == 0) launch_pass_t<R, L, DIR, true, fft_contig_group<R, L>()>(in, out, q, s);
+  else if (ef) launch_pass_t<R, L, DIR, true, 1>(in, out, q, s);
   else if (q.nv % GF == 0 && (GH == GF || strided_group<R>() == FftCfg<R>::W))
     launch_pass_t<R, L, DIR, false, GF>(in, out, q, s);
   else launch_pass_t<R, L, DIR, false, GH>(in, out, q, s);
@@ -448,10 +449,11 @@ bool len_ok(int L) { return L >= 64 && L <= 4096 && (L & (L - 1)) == 0; }
 // the CTA's (half) line group.
 bool fft3_supported(int d, const int* n, const int* N, bool single) {
   if (getenv("NFFTK_NO_PRUNED_FFT")) return false;
-  if (d != 3 && d != 2) return false;
+  if (d < 1 || d > 3) return false;
   const int G = single ? 8 : 4;  // the half group of the strided passes
   for (int i = 0; i < d; ++i)
     if (!len_ok(n[i]) || (N[i] & 1) || N[i] > n[i] || N[i] < 2) return false;
+  if (d == 1) return true;  // one contiguous line
   return N[d - 1] % G == 0 && n[d - 2] % G == 0;
 }
 
@@ -478,6 +480,7 @@ void fft3_twiddles(int L, bool single, std::vector<unsigned char>& out) {
 }
 
 size_t fft3_scratch_elems(const Fft3Geom& q) {
+  if (q.d == 1) return 0;
   if (q.d == 2) return (size_t)q.n[0] * q.N[1];  // T (n0 x N1)
   // T1 (n0 x N1 x N2) followed by T2 (n0 x n1 x N2)
   return (size_t)q.n[0] * q.N[1] * q.N[2] + (size_t)q.n[0] * q.n[1] * q.N[2];
@@ -584,8 +587,30 @@ static void fft3_inverse_t(const void* grid, void* scratch_a, void* scratch_b, v
   launch_pass<R>(t1, fhat, a, q.n[0], 1, false, s);
 }
 
+// d = 1: the one line, f_hat -> (padded) grid and back
+template <typename R>
+static void fft1_t(const void* in, void* out, bool forward, bool padded, const Fft3Geom& q, cudaStream_t s) {
+  FftPass c{};
+  c.nu = 1; c.nv = 1;
+  c.in_se = 1; c.out_se = 1;
+  c.in_band = forward ? q.N[0] : 0;
+  c.out_band = forward ? 0 : q.N[0];
+  c.scale_in = forward; c.scale_out = !forward;
+  c.scale = 1.0 / q.grid_size; c.col_e = q.icol[0]; c.col_u = nullptr; c.col_v = nullptr;
+  c.pad_m = forward && padded ? q.m : -1; c.pad_d = 1;
+  for (int i = 0; i < 3; ++i) { c.pad_n[i] = 1; c.pad_np[i] = 1; }
+  c.pad_n[2] = q.n[0]; c.pad_np[2] = q.np[0];
+  c.tw = q.tw[0];
+  launch_pass<R>(in, out, c, q.n[0], forward ? -1 : 1, true, s);
+}
+
 void fft3_forward(bool single, const void* fhat, void* scratch, void* out, bool padded, const Fft3Geom& q,
                   cudaStream_t s) {
+  if (q.d == 1) {
+    if (single) fft1_t<float>(fhat, out, true, padded, q, s);
+    else fft1_t<double>(fhat, out, true, padded, q, s);
+    return;
+  }
   if (q.d == 2) {
     if (single) fft2_forward_t<float>(fhat, scratch, out, padded, q, s);
     else fft2_forward_t<double>(fhat, scratch, out, padded, q, s);
@@ -597,6 +622,11 @@ void fft3_forward(bool single, const void* fhat, void* scratch, void* out, bool 
 
 void fft3_inverse(bool single, const void* grid, void* scratch_a, void* scratch_b, void* fhat,
                   const Fft3Geom& q, cudaStream_t s) {
+  if (q.d == 1) {
+    if (single) fft1_t<float>(grid, fhat, false, false, q, s);
+    else fft1_t<double>(grid, fhat, false, false, q, s);
+    return;
+  }
   if (q.d == 2) {
     if (single) fft2_inverse_t<float>(grid, scratch_a, fhat, q, s);
     else fft2_inverse_t<double>(grid, scratch_a, fhat, q, s);

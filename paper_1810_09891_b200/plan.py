@@ -366,7 +366,7 @@ class Plan:
     def fft(self):
         """Extension: how a ready plan runs F / F^H -- "pruned" (fft.cu: three
         passes of line FFTs over the N-band only, with D, D^H and the ghost
-        padding fused in; d=2, 3 with power-of-two n_i <= 4096) or "cufft" (dense n-grid)."""
+        padding fused in; power-of-two n_i of 64..4096) or "cufft" (dense n-grid)."""
         return ("cufft", "pruned")[int(self._params()[15])]
 
     @property

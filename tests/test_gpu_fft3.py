@@ -163,3 +163,15 @@ def test_pruned_fft_d2_longer_lines_take_cufft(oracle):
     assert path == "cufft"
     assert e2(oracle.trafo(N, n, m, x, fh), f) < 1e-12
     assert e2(oracle.adjoint(N, n, m, x, fs), a) < 1e-12
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("N,n,m", [((1024,), (2048,), 8), ((32,), (64,), 4), ((100,), (128,), 6),
+                                   ((2048,), (4096,), 3), ((2,), (512,), 2)])
+def test_pruned_fft_d1_matches_oracle(N, n, m, precision, oracle):
+    """d = 1: one fused pass each way (f_hat -> padded grid, grid -> f_hat)."""
+    M = 3000
+    x, fh, fs, (path, f, a) = run(N, n, m, M, precision)
+    assert path == "pruned"
+    assert e2(oracle.trafo(N, n, m, x, fh), f) < TOL[precision]
+    assert e2(oracle.adjoint(N, n, m, x, fs), a) < TOL[precision]
