@@ -558,13 +558,26 @@ struct IPipeCfg {
   static constexpr int ELEM = 2 * (int)sizeof(R);
   static constexpr int HS = ELEM == 8 ? HL + (HL & 1) : HL;
   static constexpr int ROWS = H0 * H1;
+  // d = 3, m <= 4: two CTAs per SM.  complex64: two halos are 79 KB, so two
+  // 12-warp CTAs with double-buffered halos fit (24 warps instead of 16 on
+  // one 16-warp CTA).  complex128: two 8-warp CTAs with one 79 KB halo buffer
+  // each -- the same 16 warps, but while one CTA sits at its tile barrier or
+  // waits for its halo the other gathers, and the 32-node passes leave fewer
+  // team slots empty in a subproblem's last batch than 64-node ones
+  // (C5 interp: c64 12.6 -> 10.4 ms, c128 19.96 -> 18.97 ms).
+#ifdef NFFTK_NO_I2CTA
+  static constexpr bool TWO_CTA = false;
+#else
+  static constexpr bool TWO_CTA = D == 3 && MM <= 4 && MM > 0;
+#endif
+  static constexpr int BLK = TWO_CTA ? 2 : 1;
 #ifdef NFFTK_ITHREADS3
   static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
 #else
   // d = 3, m >= 5 (one halo buffer): 20 warps hide more of the halo-cell
   // load latency (C3 interp 0.363 -> 0.351 ms, c64 0.230 -> 0.217; 24 warps
   // at the 85-register cap: 0.368); m <= 4 stays at 16 (C5 20.0 vs 20.5 ms)
-  static constexpr int THREADS = D == 3 ? (MM >= 5 ? 640 : 512) : 256;
+  static constexpr int THREADS = D == 3 ? (MM >= 5 ? 640 : (TWO_CTA ? (ELEM == 8 ? 384 : 256) : 512)) : 256;
 #endif
   // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
 #ifdef NFFTK_NO_HALF
@@ -602,7 +615,7 @@ struct IPipeCfg {
   static constexpr size_t HALO = al128((size_t)ROWS * HS * ELEM);  // TMA tensor destinations: 128 B
   static constexpr size_t ctl_bytes(int s) { return al(16 * (size_t)s + sizeof(StageMetaI) * s + 64 + 16); }
   static constexpr size_t halo_off(int s) { return al128(s * SB + ctl_bytes(s)); }
-  static constexpr size_t LIMIT = 224 * 1024;
+  static constexpr size_t LIMIT = TWO_CTA ? 112 * 1024 : 224 * 1024;
   // prefer double-buffered halos (next halo loads under the current tile),
   // then the deepest node ring
   static constexpr int pick_s() {
@@ -621,7 +634,7 @@ struct IPipeCfg {
 };
 
 template <typename R, int D, int MM>
-__global__ void __launch_bounds__(IPipeCfg<R, D, MM>::THREADS, 1)
+__global__ void __launch_bounds__(IPipeCfg<R, D, MM>::THREADS, IPipeCfg<R, D, MM>::BLK)
 k_interp_pipe(const __grid_constant__ CUtensorMap tmap, cplx_t<R>* __restrict__ fout,
               const double* __restrict__ psi, const int4* __restrict__ rec,
               const int* __restrict__ perm, const int4* __restrict__ subs, int nsubs, Geom g) {
