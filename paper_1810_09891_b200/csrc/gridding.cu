@@ -567,17 +567,24 @@ struct IPipeCfg {
   // (C5 interp: c64 12.6 -> 10.4 ms, c128 19.96 -> 18.97 ms).
 #ifdef NFFTK_NO_I2CTA
   static constexpr bool TWO_CTA = false;
+#elif defined(NFFTK_I2CTA_M6)
+  static constexpr bool TWO_CTA = D == 3 && MM > 0 && (MM <= 4 || ELEM == 8);  // A/B: c64 m >= 5 too
 #else
   static constexpr bool TWO_CTA = D == 3 && MM <= 4 && MM > 0;
 #endif
+#ifdef NFFTK_I2_BLK
+  static constexpr int BLK = TWO_CTA ? 2 : (D == 2 ? NFFTK_I2_BLK : 1);  // A/B: register cap for d = 2
+#else
   static constexpr int BLK = TWO_CTA ? 2 : 1;
+#endif
 #ifdef NFFTK_ITHREADS3
   static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
 #else
   // d = 3, m >= 5 (one halo buffer): 20 warps hide more of the halo-cell
   // load latency (C3 interp 0.363 -> 0.351 ms, c64 0.230 -> 0.217; 24 warps
   // at the 85-register cap: 0.368); m <= 4 stays at 16 (C5 20.0 vs 20.5 ms)
-  static constexpr int THREADS = D == 3 ? (MM >= 5 ? 640 : (TWO_CTA ? (ELEM == 8 ? 384 : 256) : 512)) : 256;
+  static constexpr int THREADS =
+      D == 3 ? (MM >= 5 ? (TWO_CTA ? 320 : 640) : (TWO_CTA ? (ELEM == 8 ? 384 : 256) : 512)) : 256;
 #endif
   // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
 #ifdef NFFTK_NO_HALF
