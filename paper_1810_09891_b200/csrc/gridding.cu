@@ -567,16 +567,18 @@ struct IPipeCfg {
   // (C5 interp: c64 12.6 -> 10.4 ms, c128 19.96 -> 18.97 ms).
 #ifdef NFFTK_NO_I2CTA
   static constexpr bool TWO_CTA = false;
-#elif defined(NFFTK_I2CTA_M6)
-  static constexpr bool TWO_CTA = D == 3 && MM > 0 && (MM <= 4 || ELEM == 8);  // A/B: c64 m >= 5 too
 #else
-  static constexpr bool TWO_CTA = D == 3 && MM <= 4 && MM > 0;
+  // complex64 at m >= 5 (one 74 KB halo buffer per CTA, 10 warps each): C3
+  // c64 interp 0.207 -> 0.191 ms; complex128 at m >= 5 has 148 KB halos
+  static constexpr bool TWO_CTA = D == 3 && MM > 0 && (MM <= 4 || ELEM == 8);
 #endif
-#ifdef NFFTK_I2_BLK
-  static constexpr int BLK = TWO_CTA ? 2 : (D == 2 ? NFFTK_I2_BLK : 1);  // A/B: register cap for d = 2
-#else
-  static constexpr int BLK = TWO_CTA ? 2 : 1;
+  // d = 2: halos and ring take 51 KB, so four 8-warp CTAs fit once the
+  // registers are capped at 64 (96 / two CTAs before): C4 interp 2.23 -> 1.87
+  // ms (c64 1.39 -> 1.25; a cap for three CTAs: 1.96 / 1.39)
+#ifndef NFFTK_I2_BLK
+#define NFFTK_I2_BLK 4
 #endif
+  static constexpr int BLK = TWO_CTA ? 2 : (D == 2 ? NFFTK_I2_BLK : 1);
 #ifdef NFFTK_ITHREADS3
   static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
 #else
