@@ -22,6 +22,7 @@ for c in ${PROFILE_CONFIGS:-C5}; do
   python tools/ncu_mix.py gpurun_out/full_$c.ncu-rep k_spread $c > gpurun_out/mix_spread_$c.txt 2>&1
   python tools/ncu_mix.py gpurun_out/full_$c.ncu-rep k_interp $c > gpurun_out/mix_interp_$c.txt 2>&1
   python tools/ncu_hot.py gpurun_out/full_$c.ncu-rep k_interp 60 > gpurun_out/hot_interp_$c.txt 2>&1
+  [ -n "$KEEP_REP" ] || rm -f gpurun_out/full_$c.ncu-rep   # gpurun_out/ only travels back under 64 MiB
 done
 for c in ${BENCH_CONFIGS:-C1 C2 C3 C4}; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_$c.log 2>&1; done
 for c in ${BENCH_C64:-C3 C4 C5}; do timeout 600 python bench.py --config $c --precision single --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_c64.log 2>&1; done
