@@ -579,6 +579,12 @@ struct IPipeCfg {
 #define NFFTK_I2_BLK 4
 #endif
   static constexpr int BLK = TWO_CTA ? 2 : (D == 2 ? NFFTK_I2_BLK : 1);
+#ifndef NFFTK_IT_C64
+#define NFFTK_IT_C64 384
+#endif
+#ifndef NFFTK_IT_C128
+#define NFFTK_IT_C128 320
+#endif
 #ifdef NFFTK_ITHREADS3
   static constexpr int THREADS = D == 3 ? NFFTK_ITHREADS3 : 256;
 #else
@@ -586,7 +592,7 @@ struct IPipeCfg {
   // load latency (C3 interp 0.363 -> 0.351 ms, c64 0.230 -> 0.217; 24 warps
   // at the 85-register cap: 0.368); m <= 4 stays at 16 (C5 20.0 vs 20.5 ms)
   static constexpr int THREADS =
-      D == 3 ? (MM >= 5 ? (TWO_CTA ? 320 : 640) : (TWO_CTA ? (ELEM == 8 ? 384 : 256) : 512)) : 256;
+      D == 3 ? (MM >= 5 ? (TWO_CTA ? 320 : 640) : (TWO_CTA ? (ELEM == 8 ? NFFTK_IT_C64 : NFFTK_IT_C128) : 512)) : 256;
 #endif
   // c64 d = 3: half-row lanes (interp_node3_half), teams of 16
 #ifdef NFFTK_NO_HALF
