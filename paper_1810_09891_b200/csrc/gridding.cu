@@ -1320,7 +1320,15 @@ struct PipeCfg {
   static constexpr int HB = (H + RPT - 1) / RPT;              // row groups per a-line
   static constexpr int GROUPS = H * HB;
   static constexpr int THREADS = (GROUPS + 31) / 32 * 32;
+  // two CTAs per SM: complex128 at m <= 4 (run-window accumulators, below);
+  // complex64 at every m -- its whole-row accumulators are fp32 (72 registers
+  // at m = 6, 80 at m = 5: no spills under the two-CTA cap) and its staging
+  // rows half the size: C3 c64 spread 0.254 -> 0.188 ms
+#ifdef NFFTK_NO_SPREAD_C64_2CTA
   static constexpr int BLOCKS = THREADS * 2 * 102 <= 65536 && MM <= 4 ? 2 : 1;
+#else
+  static constexpr int BLOCKS = (THREADS * 2 * 102 <= 65536 && MM <= 4) || sizeof(R) == 4 ? 2 : 1;
+#endif
   // Register budget of 2 CTAs/SM: run-window accumulators (K cells, the
   // factor loads of a node all in flight) instead of the whole halo row
   // (measured C5 spread 52.2 -> 41.8 ms; the whole-row switch stays 5% faster
